@@ -1,0 +1,350 @@
+"""bench.py -- throughput of the hot path on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+A step = one pass of the whole hot path over one batch: the per-GPU shard of
+BASELINE.json configs[4] (the bulk sharded run: 2^31 fp64 normals from 2^16 LFG streams
+per GPU, seed 11, mu 0, sigma 1) generated once by each method B1, B2, B3 and Polar P
+(seeding a1 is the one-time nrng_create, reported apart).
+Weak scaling: rank r owns global streams [r 2^16, (r+1) 2^16) -- at 8 GPUs this is
+exactly configs[4] (2^34 normals over 2^19 streams).  Generation needs no communication;
+NCCL all-reduces only the validation moments/histograms, after the timed region.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1004_3105_b200 import workloads as W  # noqa: E402
+
+METRIC = "fp64 normals/sec per method (B1, B3, Polar) at 1/2/4/8 B200; % of roofline"
+METHODS = ("B1", "B2", "B3", "P")
+CFG = W.C5_SHARD
+BYTES_PER_NORMAL = 8  # algorithmic HBM traffic: one fp64 written per normal
+# Algorithmic FP64 work per normal: the paper's operation tallies
+# (B1 P:98-101, P P:131-134, B3 P:280-295, B2 P:159-170) priced per primitive in DP-pipe
+# instructions of the sm_100a libdevice fast paths (ln 28, sqrt 8, div 8, sincospi 24,
+# sincos16 21, Horner-15 15, uniform 2) -- SURVEY.md §8(a).
+DP_PER_NORMAL = {"B1": 34.5, "B2": 33.0, "B3": 30.5, "P": 28.5}
+FP64_PEAK_NOMINAL = 148 * 64 * 1.965e9  # DP lanes per SM x SMs x max clock (DP instr/s)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + self.FIELDS,
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[0]) for r in rows if len(r) >= 8 and r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 8 and r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 8:
+                continue
+            for nm, v in zip(names, r[4:8]):
+                if v.strip() == "Active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_sample(streams_per_method: int, threads: int):
+    """Time the CPU oracle, as it stands, on a bounded sample of the same workload: the first
+    `streams_per_method` streams of the shard, each with the full per-stream quota
+    (2^14 pairs), once per method.  Streams are independent with equal quotas, so the
+    sample has the workload's exact per-stream shape."""
+    import oracle as O
+
+    O.set_threads(threads)
+    per_stream = CFG.n // CFG.streams
+    n = streams_per_method * per_stream
+    total, secs = 0, 0.0
+    per = {}
+    for m in METHODS:
+        st = O.Streams(CFG.seed, streams_per_method)
+        t0 = time.perf_counter()
+        if m == "P":
+            st.normal_polar(n, CFG.mu, CFG.sigma)
+        else:
+            st.normal_boxmuller(n, CFG.mu, CFG.sigma, int(m[1]))
+        dt = time.perf_counter() - t0
+        per[m] = n / dt
+        total += n
+        secs += dt
+    return total / secs, per, n, secs
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample_streams = args.ref_streams
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, per, n, secs = oracle_sample(sample_streams, threads)
+        if i >= args.warmup:
+            vals.append((v, per, secs))
+    value = float(np.mean([v for v, _, _ in vals]))
+    sample = ("%d streams x 2^14 pairs (the shard's per-stream quota) per method, %d normals per method, "
+              "first streams of the seed-11 shard" % (sample_streams, sample_streams * (CFG.n // CFG.streams)))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "normals/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * float(np.mean([s for _, _, s in vals])),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(args.gpus),
+        "per_method": {m: float(np.mean([p[m] for _, p, _ in vals])) for m in METHODS},
+        "cpu_baseline": {"value": value, "unit": "normals/s", "cores": threads, "kind": "oracle",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "normals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(n_gpus):
+    return {"workload": "BASELINE configs[4] per-GPU shard: 2^31 fp64 normals/GPU from 2^16 LFG(607,273) "
+                        "streams/GPU (global ids [r*2^16,(r+1)*2^16)), seed 11, mu 0, sigma 1; one call per "
+                        "method B1,B2,B3,P per step",
+            "methods": list(METHODS), "n_per_gpu_per_method": CFG.n, "streams_per_gpu": CFG.streams,
+            "seed": CFG.seed, "mu": CFG.mu, "sigma": CFG.sigma, "parallelism": "stream-sharded x%d" % n_gpus,
+            "l2": "no flush needed: per call the 318 MB LFG state and 16 GiB output exceed the 126 MB L2"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-streams", type=int, default=4096)
+    ap.add_argument("--validate", type=int, default=1)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1004_3105_b200 as P
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    t0 = time.perf_counter()
+    g = P.Generator(CFG.seed, CFG.streams, first_stream=rank * CFG.streams)
+    torch.cuda.synchronize()
+    create_s = time.perf_counter() - t0
+    out = torch.empty(CFG.n, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        for i, m in enumerate(METHODS):
+            if evs is not None:
+                evs[i][0].record(stream)
+            g.normal(m, out=out, mu=CFG.mu, sigma=CFG.sigma)
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    clocks = Clocks(local)
+    launches0 = g.kernel_launches
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in METHODS]
+           for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record(stream)
+    for s in range(args.steps):
+        step(evs[s])
+    end.record(stream)
+    barrier()
+    clk = clocks.stop()
+    launches = g.kernel_launches - launches0
+    elapsed = start.elapsed_time(end)
+    per_ms = {m: float(np.mean([evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(args.steps)]))
+              for i, m in enumerate(METHODS)}
+    t = torch.tensor([elapsed] + [per_ms[m] for m in METHODS], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t[0])
+    per_ms = {m: float(t[1 + i]) for i, m in enumerate(METHODS)}
+    total_normals = world * len(METHODS) * CFG.n * args.steps
+    value = total_normals / (elapsed / 1e3)
+
+    # ---- validation: moments + histogram per method, all-reduced over NCCL (the only exchange)
+    validation = {}
+    if args.validate:
+        from statistics import NormalDist
+
+        K = 256
+        edges = [CFG.mu + CFG.sigma * NormalDist().inv_cdf(i / K) for i in range(1, K)]
+        for m in METHODS:
+            g.normal(m, out=out, mu=CFG.mu, sigma=CFG.sigma)
+            sums, hist = P.stats(out, CFG.mu, edges)
+            red = torch.cat([sums[:4], hist.to(torch.float64)])
+            mn, mx = sums[4:5].clone(), sums[5:6].clone()
+            if world > 1:
+                dist.all_reduce(red)
+                dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+                dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            red = red.cpu().numpy()
+            n = world * CFG.n
+            m1 = red[0] / n
+            var = red[1] / n - m1 * m1
+            skew = (red[2] / n - 3 * m1 * red[1] / n + 2 * m1**3) / var**1.5
+            kurt = (red[3] / n) / var**2 - 3
+            hist_v = red[4:]
+            chi2 = float(np.sum((hist_v - n / K) ** 2 / (n / K)))
+            ok = (abs(m1) < 4 / math.sqrt(n) and abs(var - 1) < 4 * math.sqrt(2 / n)
+                  and abs(skew) < 4 * math.sqrt(6 / n) and abs(kurt) < 4 * math.sqrt(24 / n))
+            validation[m] = {"mean": m1, "var": var, "skew": skew, "exkurt": kurt, "chi2": chi2, "dof": K - 1,
+                             "min": float(mn), "max": float(mx), "moments_4se_pass": bool(ok)}
+
+    # ---- e2e: the same step through the public API with HOST output buffers (pinned),
+    # the device->host copies inside the timed region (library chunked/overlapped path)
+    e2e = None
+    if not args.no_e2e:
+        hbuf = torch.empty(CFG.n, dtype=torch.float64).pin_memory()
+        ge = P.Generator(CFG.seed, CFG.streams, first_stream=rank * CFG.streams)
+        for m in METHODS:
+            ge.normal(m, out=hbuf, mu=CFG.mu, sigma=CFG.sigma)
+        barrier()
+        te = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for m in METHODS:
+                ge.normal(m, out=hbuf, mu=CFG.mu, sigma=CFG.sigma)
+        barrier()
+        te = torch.tensor([time.perf_counter() - te], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ev = world * len(METHODS) * CFG.n * args.e2e_steps / float(te)
+        e2e = {"value": ev, "unit": "normals/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": len(METHODS) * CFG.n * 8,
+               "note": "host wall clock (host-blocking API call), pinned host output; %d steps" % args.e2e_steps}
+        ge.close()
+        del hbuf
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_kind = load_peaks()
+    dom = max(METHODS, key=lambda m: per_ms[m])
+    t_launch = per_ms[dom] / 1e3
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_achieved = BYTES_PER_NORMAL * CFG.n / t_launch / 1e9
+    fp64_peak = FP64_PEAK_NOMINAL
+    fp64_achieved = DP_PER_NORMAL[dom] * CFG.n / t_launch
+    t_hbm = BYTES_PER_NORMAL * CFG.n / (hbm_peak * 1e9)
+    t_fp64 = DP_PER_NORMAL[dom] * CFG.n / fp64_peak
+    if t_fp64 >= t_hbm:
+        roof = {"bound": "alu", "achieved": fp64_achieved / 1e12, "peak": fp64_peak / 1e12,
+                "unit": "T DP-pipe instr/s", "frac": fp64_achieved / fp64_peak, "traffic": None,
+                "kernel": "%s (%s)" % ({"P": "polar_kernel"}.get(dom, "bm_kernel<%s>" % dom[1]), dom),
+                "peak_source": "148 SMs x 64 FP64 lanes x 1965 MHz (nominal; measured DFMA 17.09 T/s)",
+                "alt_hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                            "frac": hbm_achieved / hbm_peak, "peak_source": peak_kind}}
+    else:
+        roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm_achieved / hbm_peak, "traffic": None, "peak_source": peak_kind}
+
+    cpu = None
+    if not args.no_cpu:
+        threads = os.cpu_count() or 1
+        # calibrate on 256 streams, then size the sample for ~10 s of oracle wall time
+        cv, _, _, csecs = oracle_sample(256, threads)
+        ns = int(min(CFG.streams, max(256, 256 * 10.0 / max(csecs, 1e-3))))
+        ns = 1 << int(math.log2(ns))
+        cv, cper, cn, csecs = oracle_sample(ns, threads)
+        cpu = {"value": cv, "unit": "normals/s", "cores": threads, "kind": "oracle",
+               "sample": "%d streams x 2^14 pairs per method (B1,B2,B3,P) = %d normals per method, %.1f s wall"
+                         % (ns, cn, csecs),
+               "per_method": cper, "cpu": cpu_model()}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "normals/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(world),
+        "per_method": {m: {"normals_per_s": world * CFG.n / (per_ms[m] / 1e3), "ms_per_call": per_ms[m],
+                           "dp_frac_of_nominal": DP_PER_NORMAL[m] * CFG.n / (per_ms[m] / 1e3) / fp64_peak,
+                           "hbm_write_frac": BYTES_PER_NORMAL * CFG.n / (per_ms[m] / 1e3) / 1e9 / hbm_peak}
+                       for m in METHODS},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        "create_s": create_s, "validation": validation,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

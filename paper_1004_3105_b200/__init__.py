@@ -1,0 +1,296 @@
+"""paper_1004_3105_b200 -- B200-native bulk fp64 normal generators (Brent 1993: B1/B2/B3, Polar).
+
+Thin Python binding over the C ABI of ``libnrng.so`` (``include/nrng.h``):
+argument marshalling only.  Every step of the method runs in the sm_100a kernels;
+PyTorch supplies device memory, CUDA streams and process groups.  There is no CPU
+fallback: if ``libnrng.so`` is missing or no CUDA device is usable, calls raise.
+
+The low-level functions carry the C names (``nrng_create``, ``nrng_normal_boxmuller``,
+...).  ``Generator`` wraps a handle for torch users.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libnrng.so")
+
+NRNG_DEFAULT, NRNG_B1, NRNG_B2, NRNG_B3, NRNG_POLAR = 0, 1, 2, 3, 4
+NRNG_OK, NRNG_EINVAL, NRNG_ENOMEM, NRNG_ECUDA, NRNG_ENODEV = 0, -1, -2, -3, -4
+LAG_R = 607
+METHODS = {"B1": 1, "B2": 2, "B3": 3, "P": 4}
+
+# name -> (argtypes, restype); mirrors include/nrng.h one to one
+_u64, _u32, _dbl, _p, _int, _sz = C.c_uint64, C.c_uint32, C.c_double, C.c_void_p, C.c_int, C.c_size_t
+SIGNATURES = {
+    "nrng_create": ([_u64, _u32, _int], _p),
+    "nrng_create_range": ([_u64, _u64, _u32, _int], _p),
+    "nrng_destroy": ([_p], None),
+    "nrng_set_stream": ([_p, _p], _int),
+    "nrng_normal_boxmuller": ([_p, _p, _sz, _dbl, _dbl, _int], _int),
+    "nrng_normal_polar": ([_p, _p, _sz, _dbl, _dbl], _int),
+    "nrng_last_error": ([], _int),
+    "nrng_error_string": ([_int], C.c_char_p),
+    "nrng_num_streams": ([_p], _u32),
+    "nrng_first_stream": ([_p], _u64),
+    "nrng_stream_counts": ([_p, _p], _int),
+    "nrng_get_state": ([_p, _p, _p], _int),
+    "nrng_set_state": ([_p, _p, _p], _int),
+    "nrng_synchronize": ([_p], _int),
+    "nrng_kernel_launches": ([_p], _u64),
+    "nrng_uniform": ([_p, _p, _sz], _int),
+    "nrng_polar_mask": ([_p, _p, _sz], _int),
+    "nrng_transform_from_uniforms": ([_p, _sz, _p, _p, _dbl, _dbl, _int, _p], _int),
+    "nrng_stats": ([_p, _sz, _dbl, _p, _int, _p, _p, _p], _int),
+}
+
+_lib = None
+
+
+class NrngError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__("%s failed: %s (%d)" % (what, _errstr(code), code))
+        self.code = code
+
+
+def lib():
+    """Load libnrng.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libnrng.so not built: run `python -m paper_1004_3105_b200.build` "
+                              "(no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _errstr(code: int) -> str:
+    try:
+        return lib().nrng_error_string(code).decode()
+    except Exception:  # pragma: no cover
+        return "error"
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != NRNG_OK:
+        raise NrngError(rc, what)
+
+
+# ------------------------------------------------------------------ C-named wrappers
+def nrng_create(seed: int, n_streams: int, variant: int = 0) -> int:
+    h = lib().nrng_create(seed, n_streams, variant)
+    if not h:
+        raise NrngError(lib().nrng_last_error(), "nrng_create")
+    return h
+
+
+def nrng_create_range(seed: int, first_stream: int, n_streams: int, variant: int = 0) -> int:
+    h = lib().nrng_create_range(seed, first_stream, n_streams, variant)
+    if not h:
+        raise NrngError(lib().nrng_last_error(), "nrng_create_range")
+    return h
+
+
+def nrng_destroy(h) -> None:
+    lib().nrng_destroy(h)
+
+
+def nrng_set_stream(h, cuda_stream: int) -> None:
+    _check(lib().nrng_set_stream(h, cuda_stream), "nrng_set_stream")
+
+
+def nrng_normal_boxmuller(h, out_ptr: int, n: int, mu: float, sigma: float, variant: int = 0) -> None:
+    _check(lib().nrng_normal_boxmuller(h, out_ptr, n, mu, sigma, variant), "nrng_normal_boxmuller")
+
+
+def nrng_normal_polar(h, out_ptr: int, n: int, mu: float, sigma: float) -> None:
+    _check(lib().nrng_normal_polar(h, out_ptr, n, mu, sigma), "nrng_normal_polar")
+
+
+def nrng_uniform(h, out_ptr: int, n: int) -> None:
+    _check(lib().nrng_uniform(h, out_ptr, n), "nrng_uniform")
+
+
+def nrng_polar_mask(h, mask_ptr: int, cand_per_stream: int) -> None:
+    _check(lib().nrng_polar_mask(h, mask_ptr, cand_per_stream), "nrng_polar_mask")
+
+
+def nrng_transform_from_uniforms(u_ptr, n_pairs, out_ptr, mask_ptr, mu, sigma, method, stream) -> None:
+    _check(lib().nrng_transform_from_uniforms(u_ptr, n_pairs, out_ptr, mask_ptr, mu, sigma, method, stream),
+           "nrng_transform_from_uniforms")
+
+
+def nrng_stats(x_ptr, n, center, edges_ptr, K, sums_ptr, hist_ptr, stream) -> None:
+    _check(lib().nrng_stats(x_ptr, n, center, edges_ptr, K, sums_ptr, hist_ptr, stream), "nrng_stats")
+
+
+def nrng_last_error() -> int:
+    return lib().nrng_last_error()
+
+
+def nrng_error_string(code: int) -> str:
+    return _errstr(code)
+
+
+def nrng_num_streams(h) -> int:
+    return lib().nrng_num_streams(h)
+
+
+def nrng_first_stream(h) -> int:
+    return lib().nrng_first_stream(h)
+
+
+def nrng_synchronize(h) -> None:
+    _check(lib().nrng_synchronize(h), "nrng_synchronize")
+
+
+def nrng_kernel_launches(h) -> int:
+    return int(lib().nrng_kernel_launches(h))
+
+
+def nrng_stream_counts(h) -> np.ndarray:
+    out = np.empty(nrng_num_streams(h), np.uint64)
+    _check(lib().nrng_stream_counts(h, out.ctypes.data), "nrng_stream_counts")
+    return out
+
+
+def nrng_get_state(h):
+    S = nrng_num_streams(h)
+    ring = np.empty((S, LAG_R), np.uint64)
+    cnt = np.empty(S, np.uint64)
+    _check(lib().nrng_get_state(h, ring.ctypes.data, cnt.ctypes.data), "nrng_get_state")
+    return ring, cnt
+
+
+def nrng_set_state(h, ring: np.ndarray, counts: np.ndarray) -> None:
+    ring = np.ascontiguousarray(ring, np.uint64)
+    counts = np.ascontiguousarray(counts, np.uint64)
+    _check(lib().nrng_set_state(h, ring.ctypes.data, counts.ctypes.data), "nrng_set_state")
+
+
+# ------------------------------------------------------------------ torch-facing API
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_ptr(torch):
+    return torch.cuda.current_stream().cuda_stream
+
+
+class Generator:
+    """A set of LFG streams [first_stream, first_stream + n_streams) on the current CUDA device.
+
+    Outputs are torch float64 tensors (device by default) or caller buffers: a CUDA
+    tensor, or a CPU tensor / numpy array (the library's host-output path).
+    """
+
+    def __init__(self, seed: int, n_streams: int, variant: int = 1, first_stream: int = 0):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1004_3105_b200 needs a CUDA device (no CPU fallback)")
+        self.seed, self.S, self.first, self.variant = int(seed), int(n_streams), int(first_stream), int(variant)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.h = nrng_create_range(self.seed, self.first, self.S, self.variant)
+        nrng_set_stream(self.h, _stream_ptr(torch))
+
+    def close(self):
+        if getattr(self, "h", None):
+            nrng_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _sync_stream(self):
+        nrng_set_stream(self.h, _stream_ptr(_torch()))
+
+    def _out(self, n, out, dtype=None):
+        torch = _torch()
+        if out is None:
+            out = torch.empty(n, dtype=dtype or torch.float64, device=self.device)
+        if isinstance(out, np.ndarray):
+            return out, out.ctypes.data, out.size
+        return out, out.data_ptr(), out.numel()
+
+    def normal_boxmuller(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, variant: int = 0, out=None):
+        out, ptr, n = self._out(n, out)
+        self._sync_stream()
+        nrng_normal_boxmuller(self.h, ptr, n, mu, sigma, variant)
+        return out
+
+    def normal_polar(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
+        out, ptr, n = self._out(n, out)
+        self._sync_stream()
+        nrng_normal_polar(self.h, ptr, n, mu, sigma)
+        return out
+
+    def normal(self, method: str, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
+        if method == "P":
+            return self.normal_polar(n, mu, sigma, out=out)
+        return self.normal_boxmuller(n, mu, sigma, METHODS[method], out=out)
+
+    def uniform(self, n: int = None, out=None):
+        out, ptr, n = self._out(n, out)
+        self._sync_stream()
+        nrng_uniform(self.h, ptr, n)
+        return out
+
+    def polar_mask(self, cand_per_stream: int):
+        torch = _torch()
+        m = torch.empty(self.S * cand_per_stream, dtype=torch.uint8, device=self.device)
+        self._sync_stream()
+        nrng_polar_mask(self.h, m.data_ptr(), cand_per_stream)
+        return m
+
+    def stream_counts(self) -> np.ndarray:
+        return nrng_stream_counts(self.h)
+
+    def get_state(self):
+        return nrng_get_state(self.h)
+
+    def set_state(self, ring, counts):
+        nrng_set_state(self.h, ring, counts)
+
+    def synchronize(self):
+        nrng_synchronize(self.h)
+
+    @property
+    def kernel_launches(self) -> int:
+        return nrng_kernel_launches(self.h)
+
+
+def transform_from_uniforms(u, method: int, mu: float = 0.0, sigma: float = 1.0):
+    """Device transform on given uniforms: method 1/2/3 = B1/B2/B3, 4 = Polar.  Returns (out, mask)."""
+    torch = _torch()
+    per = 3 if method == 3 else 2
+    n_pairs = u.numel() // per
+    out = torch.empty(2 * n_pairs, dtype=torch.float64, device=u.device)
+    mask = torch.empty(n_pairs, dtype=torch.uint8, device=u.device) if method == 4 else None
+    nrng_transform_from_uniforms(u.data_ptr(), n_pairs, out.data_ptr(), mask.data_ptr() if mask is not None else None,
+                                 mu, sigma, method, _stream_ptr(torch))
+    return out, mask
+
+
+def stats(x, center: float, edges):
+    """Device validation reduction: (sums[6] = sum d, d^2, d^3, d^4, min, max; hist[K] int64)."""
+    torch = _torch()
+    edges = torch.as_tensor(edges, dtype=torch.float64, device=x.device).contiguous()
+    K = edges.numel() + 1
+    sums = torch.empty(6, dtype=torch.float64, device=x.device)
+    hist = torch.empty(K, dtype=torch.int64, device=x.device)
+    nrng_stats(x.data_ptr(), x.numel(), center, edges.data_ptr(), K, sums.data_ptr(), hist.data_ptr(),
+               _stream_ptr(torch))
+    return sums, hist

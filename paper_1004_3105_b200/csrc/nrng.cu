@@ -1,0 +1,415 @@
+// nrng.cu -- host side of libnrng.so: the C ABI declared in include/nrng.h.
+//
+// Argument marshalling, validation, launch geometry and the host-buffer (chunked,
+// overlapped D2H) path.  Every step of the method runs in the kernels of
+// nrng_kernels.cuh; there is no CPU fallback: without a usable CUDA device every
+// entry point fails with NRNG_ENODEV / NRNG_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "../../include/nrng.h"
+#include "nrng_kernels.cuh"
+
+using namespace nrng;
+
+namespace {
+
+thread_local int g_last = NRNG_OK;
+
+int set_err(int code) {
+    g_last = code;
+    return code;
+}
+
+int cuda_err(cudaError_t e) {
+    if (e == cudaSuccess) return set_err(NRNG_OK);
+    fprintf(stderr, "[nrng] CUDA error: %s\n", cudaGetErrorString(e));
+    return set_err(NRNG_ECUDA);
+}
+
+constexpr size_t kBmSmem = kWarpsPerBlock * kWin * sizeof(uint64_t);
+constexpr size_t kPolarSmem = kBmSmem + kWarpsPerBlock * 3 * kQueue * sizeof(double);
+constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
+constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)
+
+struct Occ {
+    int bm1 = 0, bm2 = 0, bm3 = 0, polar = 0, uni = 0, mask = 0, init = 0;
+};
+
+}  // namespace
+
+struct nrng_gen {
+    int device = 0;
+    int num_sms = 148;
+    uint64_t seed = 0, first = 0;
+    uint32_t S = 0;
+    int variant = 1;
+    uint64_t* ring = nullptr;   // S x kPitch
+    uint64_t* count = nullptr;  // S
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    double* stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev_ready[2] = {nullptr, nullptr};
+    cudaEvent_t ev_free[2] = {nullptr, nullptr};
+    uint64_t launches = 0;
+    Occ occ;
+};
+
+namespace {
+
+template <typename K>
+int occupancy(K kernel, size_t smem) {
+    int b = 0;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kWarpsPerBlock * 32, smem) != cudaSuccess) b = 1;
+    return std::max(b, 1);
+}
+
+bool check_device(nrng_handle h) {
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess) return false;
+    return d == h->device;
+}
+
+unsigned grid_for(uint32_t nstreams, int per_sm, int num_sms) {
+    uint64_t want = (nstreams + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    uint64_t cap = (uint64_t)per_sm * num_sms;
+    return (unsigned)std::max<uint64_t>(1, std::min(want, cap));
+}
+
+// Launch one bulk kernel over streams [b, e) of the handle.
+enum class Kind { BM1, BM2, BM3, POLAR, UNIFORM };
+
+cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st) {
+    uint32_t ns = p.s_end - p.s_begin;
+    switch (kind) {
+        case Kind::BM1:
+            bm_kernel<1><<<grid_for(ns, h->occ.bm1, h->num_sms), kWarpsPerBlock * 32, kBmSmem, st>>>(p);
+            break;
+        case Kind::BM2:
+            bm_kernel<2><<<grid_for(ns, h->occ.bm2, h->num_sms), kWarpsPerBlock * 32, kBmSmem, st>>>(p);
+            break;
+        case Kind::BM3:
+            bm_kernel<3><<<grid_for(ns, h->occ.bm3, h->num_sms), kWarpsPerBlock * 32, kBmSmem, st>>>(p);
+            break;
+        case Kind::POLAR:
+            polar_kernel<<<grid_for(ns, h->occ.polar, h->num_sms), kWarpsPerBlock * 32, kPolarSmem, st>>>(p);
+            break;
+        case Kind::UNIFORM:
+            uniform_kernel<<<grid_for(ns, h->occ.uni, h->num_sms), kWarpsPerBlock * 32, kBmSmem, st>>>(p);
+            break;
+    }
+    h->launches += 1;
+    return cudaGetLastError();
+}
+
+bool is_device_pointer(const void* ptr) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int ensure_staging(nrng_handle h) {
+    if (h->stage[0]) return NRNG_OK;
+    if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return NRNG_ECUDA;
+    for (int i = 0; i < 2; ++i) {
+        if (cudaMalloc(&h->stage[i], kStageDoubles * sizeof(double)) != cudaSuccess) return NRNG_ENOMEM;
+        if (cudaEventCreateWithFlags(&h->ev_ready[i], cudaEventDisableTiming) != cudaSuccess) return NRNG_ECUDA;
+        if (cudaEventCreateWithFlags(&h->ev_free[i], cudaEventDisableTiming) != cudaSuccess) return NRNG_ECUDA;
+    }
+    return NRNG_OK;
+}
+
+// Fill `n` slots (units = pairs for normals, per_unit = 2; or uniforms, per_unit = 1)
+// into `out` (device or host).  Host outputs are produced stream-range by stream-range
+// into two alternating device staging buffers; each chunk's D2H copy on the copy
+// stream overlaps the next chunk's kernel.
+int run_bulk(nrng_handle h, Kind kind, double* out, size_t n, uint64_t units, int per_unit, double mu,
+             double sigma) {
+    BulkParams p{};
+    p.ring = h->ring;
+    p.count = h->count;
+    p.units = units;
+    p.q = units / h->S;
+    p.rem = units % h->S;
+    p.n = n;
+    p.mu = mu;
+    p.sigma = sigma;
+    const uint32_t active = p.q == 0 ? (uint32_t)p.rem : h->S;  // streams with work
+    if (is_device_pointer(out)) {
+        p.out = out;
+        p.shift = 0;
+        p.aligned = ((uintptr_t)out & 15) == 0;
+        p.s_begin = 0;
+        p.s_end = active;
+        return cuda_err(launch_bulk(h, kind, p, h->stream));
+    }
+    int rc = ensure_staging(h);
+    if (rc != NRNG_OK) return set_err(rc);
+    // streams per chunk so that one chunk's slots fit a staging buffer
+    const uint64_t slots_per_stream = (p.q + 1) * per_unit;
+    const uint64_t g = std::max<uint64_t>(1, kStageDoubles / slots_per_stream);
+    auto slot_off = [&](uint64_t k) { return (k * p.q + std::min<uint64_t>(k, p.rem)) * per_unit; };
+    int buf = 0;
+    cudaError_t e = cudaSuccess;
+    for (uint64_t b = 0; b < active && e == cudaSuccess; b += g, buf ^= 1) {
+        const uint64_t en = std::min<uint64_t>(active, b + g);
+        const uint64_t lo = slot_off(b);
+        const uint64_t hi = std::min<uint64_t>(slot_off(en), n);
+        if (hi <= lo) continue;
+        e = cudaStreamWaitEvent(h->stream, h->ev_free[buf], 0);  // previous copy out of this buffer done
+        if (e != cudaSuccess) break;
+        p.out = h->stage[buf];
+        p.shift = lo;
+        p.aligned = 1;
+        p.s_begin = (uint32_t)b;
+        p.s_end = (uint32_t)en;
+        e = launch_bulk(h, kind, p, h->stream);
+        if (e != cudaSuccess) break;
+        e = cudaEventRecord(h->ev_ready[buf], h->stream);
+        if (e != cudaSuccess) break;
+        e = cudaStreamWaitEvent(h->copy_stream, h->ev_ready[buf], 0);
+        if (e != cudaSuccess) break;
+        e = cudaMemcpyAsync(out + lo, h->stage[buf], (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost,
+                            h->copy_stream);
+        if (e != cudaSuccess) break;
+        e = cudaEventRecord(h->ev_free[buf], h->copy_stream);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->copy_stream);
+    return cuda_err(e);
+}
+
+bool bad_params(double mu, double sigma) { return !std::isfinite(mu) || !std::isfinite(sigma) || sigma < 0; }
+
+nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) {
+    if (S == 0 || variant < 0 || variant > 3) {
+        set_err(NRNG_EINVAL);
+        return nullptr;
+    }
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        set_err(NRNG_ENODEV);
+        return nullptr;
+    }
+    nrng_gen* h = new (std::nothrow) nrng_gen();
+    if (!h) {
+        set_err(NRNG_ENOMEM);
+        return nullptr;
+    }
+    h->device = dev;
+    h->seed = seed;
+    h->first = first;
+    h->S = S;
+    h->variant = variant == 0 ? 1 : variant;
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    h->occ.bm1 = occupancy(bm_kernel<1>, kBmSmem);
+    h->occ.bm2 = occupancy(bm_kernel<2>, kBmSmem);
+    h->occ.bm3 = occupancy(bm_kernel<3>, kBmSmem);
+    h->occ.polar = occupancy(polar_kernel, kPolarSmem);
+    h->occ.uni = occupancy(uniform_kernel, kBmSmem);
+    h->occ.mask = occupancy(polar_mask_kernel, kBmSmem);
+    h->occ.init = occupancy(init_kernel, kInitSmem);
+    if (cudaMalloc(&h->ring, (size_t)S * kPitch * sizeof(uint64_t)) != cudaSuccess ||
+        cudaMalloc(&h->count, (size_t)S * sizeof(uint64_t)) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(h->ring);
+        delete h;
+        set_err(NRNG_ENOMEM);
+        return nullptr;
+    }
+    init_kernel<<<grid_for(S, h->occ.init, h->num_sms), kWarpsPerBlock * 32, kInitSmem, h->stream>>>(
+        h->ring, h->count, seed, first, S);
+    h->launches += 1;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) {
+        cuda_err(e);
+        cudaFree(h->ring);
+        cudaFree(h->count);
+        delete h;
+        return nullptr;
+    }
+    set_err(NRNG_OK);
+    return h;
+}
+
+}  // namespace
+
+extern "C" {
+
+nrng_handle nrng_create(uint64_t seed, uint32_t n_streams, int variant) {
+    return create_impl(seed, 0, n_streams, variant);
+}
+
+nrng_handle nrng_create_range(uint64_t seed, uint64_t first_stream, uint32_t n_streams, int variant) {
+    return create_impl(seed, first_stream, n_streams, variant);
+}
+
+void nrng_destroy(nrng_handle h) {
+    if (!h) return;
+    cudaStreamSynchronize(h->stream);
+    if (h->copy_stream) {
+        cudaStreamSynchronize(h->copy_stream);
+        cudaStreamDestroy(h->copy_stream);
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(h->stage[i]);
+        if (h->ev_ready[i]) cudaEventDestroy(h->ev_ready[i]);
+        if (h->ev_free[i]) cudaEventDestroy(h->ev_free[i]);
+    }
+    cudaFree(h->ring);
+    cudaFree(h->count);
+    delete h;
+    set_err(NRNG_OK);
+}
+
+int nrng_set_stream(nrng_handle h, void* cuda_stream) {
+    if (!h) return set_err(NRNG_EINVAL);
+    h->stream = (cudaStream_t)cuda_stream;
+    return set_err(NRNG_OK);
+}
+
+int nrng_normal_boxmuller(nrng_handle h, double* out, size_t n, double mu, double sigma, int variant) {
+    if (!h || (n > 0 && !out) || bad_params(mu, sigma) || variant < 0 || variant > 3) return set_err(NRNG_EINVAL);
+    if (!check_device(h)) return set_err(NRNG_EINVAL);
+    if (n == 0) return set_err(NRNG_OK);
+    const int v = variant == 0 ? h->variant : variant;
+    const Kind k = v == 1 ? Kind::BM1 : (v == 2 ? Kind::BM2 : Kind::BM3);
+    return run_bulk(h, k, out, n, (n + 1) / 2, 2, mu, sigma);
+}
+
+int nrng_normal_polar(nrng_handle h, double* out, size_t n, double mu, double sigma) {
+    if (!h || (n > 0 && !out) || bad_params(mu, sigma)) return set_err(NRNG_EINVAL);
+    if (!check_device(h)) return set_err(NRNG_EINVAL);
+    if (n == 0) return set_err(NRNG_OK);
+    return run_bulk(h, Kind::POLAR, out, n, (n + 1) / 2, 2, mu, sigma);
+}
+
+int nrng_uniform(nrng_handle h, double* out, size_t n) {
+    if (!h || (n > 0 && !out)) return set_err(NRNG_EINVAL);
+    if (!check_device(h)) return set_err(NRNG_EINVAL);
+    if (n == 0) return set_err(NRNG_OK);
+    return run_bulk(h, Kind::UNIFORM, out, n, n, 1, 0.0, 1.0);
+}
+
+int nrng_polar_mask(nrng_handle h, uint8_t* dev_mask, size_t cand_per_stream) {
+    if (!h || (cand_per_stream > 0 && !dev_mask)) return set_err(NRNG_EINVAL);
+    if (!check_device(h)) return set_err(NRNG_EINVAL);
+    if (cand_per_stream == 0) return set_err(NRNG_OK);
+    BulkParams p{};
+    p.ring = h->ring;
+    p.count = h->count;
+    p.s_begin = 0;
+    p.s_end = h->S;
+    polar_mask_kernel<<<grid_for(h->S, h->occ.mask, h->num_sms), kWarpsPerBlock * 32, kBmSmem, h->stream>>>(
+        p, dev_mask, cand_per_stream);
+    h->launches += 1;
+    return cuda_err(cudaGetLastError());
+}
+
+int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* dev_out, uint8_t* dev_mask, double mu,
+                                 double sigma, int method, void* cuda_stream) {
+    if ((n_pairs > 0 && (!dev_u || !dev_out)) || bad_params(mu, sigma) || method < 1 || method > 4)
+        return set_err(NRNG_EINVAL);
+    if (n_pairs == 0) return set_err(NRNG_OK);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return set_err(NRNG_ENODEV);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_pairs + 255) / 256, (uint64_t)sms * 8);
+    transform_kernel<<<grid, 256, 0, (cudaStream_t)cuda_stream>>>(dev_u, n_pairs, dev_out, dev_mask, mu, sigma,
+                                                                  method);
+    return cuda_err(cudaGetLastError());
+}
+
+int nrng_stats(const double* dev_x, size_t n, double center, const double* dev_edges, int K, double* dev_sums,
+               int64_t* dev_hist, void* cuda_stream) {
+    if (K < 2 || K > 1024 || !dev_edges || !dev_sums || !dev_hist || (n > 0 && !dev_x) || !std::isfinite(center))
+        return set_err(NRNG_EINVAL);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return set_err(NRNG_ENODEV);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const int nblocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + kStatsThreads - 1) / kStatsThreads,
+                                                                      (uint64_t)sms * 8));
+    double* partial = nullptr;
+    cudaError_t e = cudaMallocAsync(&partial, (size_t)nblocks * 6 * sizeof(double), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(dev_hist, 0, (size_t)K * sizeof(int64_t), st);
+    if (e == cudaSuccess) {
+        stats_partial_kernel<<<nblocks, kStatsThreads, 0, st>>>(dev_x, n, center, dev_edges, K, partial,
+                                                               reinterpret_cast<unsigned long long*>(dev_hist));
+        stats_final_kernel<<<1, 32, 0, st>>>(partial, nblocks, dev_sums);
+        e = cudaGetLastError();
+    }
+    if (partial) cudaFreeAsync(partial, st);
+    return cuda_err(e);
+}
+
+int nrng_last_error(void) { return g_last; }
+
+const char* nrng_error_string(int code) {
+    switch (code) {
+        case NRNG_OK: return "ok";
+        case NRNG_EINVAL: return "invalid argument";
+        case NRNG_ENOMEM: return "out of device memory";
+        case NRNG_ECUDA: return "CUDA error";
+        case NRNG_ENODEV: return "no CUDA device";
+        default: return "unknown error";
+    }
+}
+
+uint32_t nrng_num_streams(nrng_handle h) { return h ? h->S : 0; }
+uint64_t nrng_first_stream(nrng_handle h) { return h ? h->first : 0; }
+uint64_t nrng_kernel_launches(nrng_handle h) { return h ? h->launches : 0; }
+
+int nrng_synchronize(nrng_handle h) {
+    if (!h) return set_err(NRNG_EINVAL);
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e == cudaSuccess && h->copy_stream) e = cudaStreamSynchronize(h->copy_stream);
+    return cuda_err(e);
+}
+
+int nrng_stream_counts(nrng_handle h, uint64_t* host_counts) {
+    if (!h || !host_counts) return set_err(NRNG_EINVAL);
+    cudaError_t e = cudaMemcpyAsync(host_counts, h->count, (size_t)h->S * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                    h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    return cuda_err(e);
+}
+
+int nrng_get_state(nrng_handle h, uint64_t* host_ring, uint64_t* host_counts) {
+    if (!h) return set_err(NRNG_EINVAL);
+    cudaError_t e = cudaSuccess;
+    if (host_ring)
+        e = cudaMemcpy2DAsync(host_ring, kLagR * sizeof(uint64_t), h->ring, kPitch * sizeof(uint64_t),
+                              kLagR * sizeof(uint64_t), h->S, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess && host_counts)
+        e = cudaMemcpyAsync(host_counts, h->count, (size_t)h->S * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                            h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    return cuda_err(e);
+}
+
+int nrng_set_state(nrng_handle h, const uint64_t* host_ring, const uint64_t* host_counts) {
+    if (!h) return set_err(NRNG_EINVAL);
+    cudaError_t e = cudaSuccess;
+    if (host_ring)
+        e = cudaMemcpy2DAsync(h->ring, kPitch * sizeof(uint64_t), host_ring, kLagR * sizeof(uint64_t),
+                              kLagR * sizeof(uint64_t), h->S, cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess && host_counts)
+        e = cudaMemcpyAsync(h->count, host_counts, (size_t)h->S * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                            h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    return cuda_err(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,344 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star): uniforms, Polar accept masks, output order, per-stream
+consumption counters and the generator state bit-exact; B1/P normals within 1e-13
+absolute; B2/B3 within 1e-13 + the paper's 1e-10 bound (reading R17) -- and
+B2's sincos16 and B3's bulk branch are in fact bit-exact given identical coefficients.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+import paper_1004_3105_b200 as P  # noqa: E402
+from paper_1004_3105_b200 import workloads as W  # noqa: E402
+
+TOL = 1e-13
+TOL_APPROX = 1e-13 + 1e-10
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1004_3105_b200 import build as B
+
+    B.build()
+    yield
+    torch.cuda.synchronize()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def gen_normals(g, method, n, mu, sigma):
+    return host(g.normal(method, n, mu, sigma))
+
+
+def ora_normals(st, method, n, mu, sigma):
+    if method == "P":
+        return st.normal_polar(n, mu, sigma)
+    return st.normal_boxmuller(n, mu, sigma, P.METHODS[method])
+
+
+def tol_for(method):
+    return TOL if method in ("B1", "P") else TOL_APPROX
+
+
+def assert_state_equal(g, st):
+    ring, cnt = g.get_state()
+    assert np.array_equal(cnt, st.counts)
+    assert np.array_equal(ring, st.rings)
+
+
+# ---------------------------------------------------------------- uniforms / state
+
+@pytest.mark.parametrize("cfg", W.ALL, ids=lambda c: c.name)
+def test_seeded_state_bit_exact(cfg):
+    g = P.Generator(cfg.seed, cfg.streams)
+    st = O.Streams(cfg.seed, cfg.streams)
+    assert_state_equal(g, st)
+
+
+@pytest.mark.parametrize("seed,S,n", [(1, 1024, 1024 * 1500 + 77), (7, 1 << 14, (1 << 14) * 70 + 5),
+                                      (42, 1 << 16, (1 << 16) * 3 + 1), (3, 37, 37 * 2000 + 36)])
+def test_uniforms_bit_exact(seed, S, n):
+    g = P.Generator(seed, S)
+    st = O.Streams(seed, S)
+    for m in (n, 3, n // 3):  # several calls: ragged tails, < S, and window reuse
+        assert np.array_equal(host(g.uniform(m)), st.uniform(m))
+    assert_state_equal(g, st)
+
+
+def test_polar_mask_bit_exact():
+    S = 1 << 14
+    g = P.Generator(7, S)
+    st = O.Streams(7, S)
+    for cand in (651, 1, 333):
+        assert np.array_equal(host(g.polar_mask(cand)), st.polar_mask(cand))
+    assert_state_equal(g, st)
+
+
+# ---------------------------------------------------------------- configs, full size
+
+def test_c1_b1_full():
+    c = W.C1
+    g, st = P.Generator(c.seed, c.streams), O.Streams(c.seed, c.streams)
+    for _ in range(2):
+        d = gen_normals(g, "B1", c.n, c.mu, c.sigma)
+        o = ora_normals(st, "B1", c.n, c.mu, c.sigma)
+        assert np.max(np.abs(d - o)) <= TOL
+    assert_state_equal(g, st)
+
+
+def test_c2_polar_full():
+    c = W.C2
+    g, st = P.Generator(c.seed, c.streams), O.Streams(c.seed, c.streams)
+    d = gen_normals(g, "P", c.n, c.mu, c.sigma)
+    o = ora_normals(st, "P", c.n, c.mu, c.sigma)
+    assert np.max(np.abs(d - o)) <= TOL  # element-wise => stream-major, accepted-pair order exact
+    assert_state_equal(g, st)  # exact stop: consumed uniforms per stream bit-exact
+
+
+@pytest.mark.parametrize("method", ["B2", "B3"])
+def test_c3_full_size_sampled_streams(method):
+    c = W.C3
+    g = P.Generator(c.seed, c.streams)
+    d = g.normal(method, c.n, c.mu, c.sigma)
+    per_stream = c.n // c.streams
+    rng = np.random.default_rng(5)
+    ks = sorted(set([0, 1, c.streams - 1] + list(rng.integers(0, c.streams, 13))))
+    counts = g.stream_counts()
+    for k in ks:
+        st = O.Streams(c.seed, 1, first_stream=int(k))
+        o = ora_normals(st, method, per_stream, c.mu, c.sigma)
+        dk = host(d[k * per_stream:(k + 1) * per_stream])
+        assert np.max(np.abs(dk - o)) <= tol_for(method)
+        assert counts[k] == st.counts[0]
+
+
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P"])
+def test_c5_shard_bench_launch_sampled(method):
+    # the exact launch bench.py times: 2^31 normals over 2^16 streams (global ids of rank 1)
+    c = W.C5_SHARD
+    first = c.streams  # rank 1 of the sharded run
+    g = P.Generator(c.seed, c.streams, first_stream=first)
+    out = torch.empty(c.n, dtype=torch.float64, device="cuda")
+    g.normal(method, out=out)
+    per_stream = c.n // c.streams
+    ks = [0, 1, 4097, 33333, c.streams - 1]
+    counts = g.stream_counts()
+    for k in ks:
+        st = O.Streams(c.seed, 1, first_stream=first + k)
+        o = ora_normals(st, method, per_stream, c.mu, c.sigma)
+        dk = host(out[k * per_stream:(k + 1) * per_stream])
+        assert np.max(np.abs(dk - o)) <= tol_for(method)
+        assert counts[k] == st.counts[0]
+    del out
+
+
+def test_c4_sweep_sequence():
+    c = W.C4
+    g, st = P.Generator(c.seed, c.streams), O.Streams(c.seed, c.streams)
+    for L in W.C4_LENGTHS:
+        for method in ("B1", "P", "B1"):
+            d = gen_normals(g, method, L, c.mu, c.sigma)
+            o = ora_normals(st, method, L, c.mu, c.sigma)
+            assert np.max(np.abs(d - o)) <= TOL, (L, method)
+    assert_state_equal(g, st)
+
+
+# ---------------------------------------------------------------- transforms on given uniforms
+
+@pytest.mark.parametrize("method", [1, 2, 3, 4])
+def test_transform_from_uniforms(method):
+    per = 3 if method == 3 else 2
+    u = W.dyadic_uniforms(100 + method, per * 300001)
+    e = W.edge_uniforms()
+    grid = np.array([[a, b] for a in e for b in e]).ravel() if per == 2 else \
+        np.array([[a, b, c] for a in e for b in e for c in e[:5]]).ravel()
+    u = np.concatenate([grid, u])
+    mu, sigma = 2.5, 0.5
+    d_out, d_mask = P.transform_from_uniforms(torch.from_numpy(u).cuda(), method, mu, sigma)
+    o_out, o_mask = O.transform_from_uniforms(u, method, mu, sigma)
+    d_out = host(d_out)
+    if method == 4:
+        assert np.array_equal(host(d_mask), o_mask)
+        acc = np.repeat(o_mask.astype(bool), 2)
+        assert np.all(np.isnan(d_out[~acc]))
+        d_out, o_out = d_out[acc], o_out[acc]
+    assert np.max(np.abs(d_out - o_out)) <= (TOL if method in (1, 4) else TOL_APPROX)
+    if method == 3:
+        # the bulk branch (u <= 8/9) has no library call: bit-exact
+        m = np.maximum(u[0::3], u[1::3])
+        bulk = np.repeat(m * m <= 8 / 9, 2)
+        assert np.array_equal(d_out[bulk], o_out[bulk])
+
+
+# ---------------------------------------------------------------- edge cases of the API
+
+def test_zero_n_is_noop_and_sigma_zero():
+    g = P.Generator(9, 64)
+    r0, c0 = g.get_state()
+    for m in ("B1", "B2", "B3", "P"):
+        assert g.normal(m, 0).numel() == 0
+    r1, c1 = g.get_state()
+    assert np.array_equal(r0, r1) and np.array_equal(c0, c1)
+    for m in ("B1", "B2", "B3", "P"):
+        x = host(g.normal(m, 1001, -4.5, 0.0))
+        assert np.all(x == -4.5)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 63, 64, 65, 127, 129, 2 * 64 * 33 + 1])
+@pytest.mark.parametrize("method", ["B1", "B3", "P"])
+def test_small_and_odd_n(n, method):
+    S = 64
+    g, st = P.Generator(4, S), O.Streams(4, S)
+    for _ in range(2):
+        d = gen_normals(g, method, n, 1.0, 2.0)
+        o = ora_normals(st, method, n, 1.0, 2.0)
+        assert d.size == n and np.max(np.abs(d - o)) <= tol_for(method)
+    assert_state_equal(g, st)
+
+
+def test_invalid_arguments():
+    g = P.Generator(1, 8)
+    out = torch.empty(16, dtype=torch.float64, device="cuda")
+    bad = [dict(mu=0.0, sigma=-1.0), dict(mu=float("nan"), sigma=1.0), dict(mu=0.0, sigma=float("inf"))]
+    r0, c0 = g.get_state()
+    for kw in bad:
+        with pytest.raises(P.NrngError) as e:
+            P.nrng_normal_boxmuller(g.h, out.data_ptr(), 16, kw["mu"], kw["sigma"], 1)
+        assert e.value.code == P.NRNG_EINVAL
+        with pytest.raises(P.NrngError):
+            P.nrng_normal_polar(g.h, out.data_ptr(), 16, kw["mu"], kw["sigma"])
+    with pytest.raises(P.NrngError):
+        P.nrng_normal_boxmuller(g.h, out.data_ptr(), 16, 0.0, 1.0, 5)
+    with pytest.raises(P.NrngError):
+        P.nrng_normal_boxmuller(g.h, None, 16, 0.0, 1.0, 1)
+    r1, c1 = g.get_state()
+    assert np.array_equal(r0, r1) and np.array_equal(c0, c1)
+
+
+def test_misaligned_device_output():
+    S, n = 32, 2 * 32 * 40
+    g, st = P.Generator(8, S), O.Streams(8, S)
+    buf = torch.empty(n + 1, dtype=torch.float64, device="cuda")
+    view = buf[1:]  # 8-byte aligned only
+    for m in ("B1", "P"):
+        g.normal(m, out=view)
+        o = ora_normals(st, m, n, 0.0, 1.0)
+        assert np.max(np.abs(host(view) - o)) <= TOL
+
+
+@pytest.mark.parametrize("method", ["B1", "B3", "P"])
+def test_host_output_path(method):
+    # out is host memory: chunked generation into staging buffers + overlapped D2H copies
+    c = W.C3
+    S, n = c.streams, (1 << 25) + 3
+    g, g2 = P.Generator(c.seed, S), P.Generator(c.seed, S)
+    h = np.empty(n)
+    g.normal(method, out=h, mu=c.mu, sigma=c.sigma)
+    pinned = torch.empty(n, dtype=torch.float64).pin_memory()
+    d = gen_normals(g2, method, n, c.mu, c.sigma)
+    assert np.array_equal(h, d)
+    g.normal(method, out=pinned, mu=c.mu, sigma=c.sigma)
+    d = gen_normals(g2, method, n, c.mu, c.sigma)
+    assert np.array_equal(pinned.numpy(), d)
+    assert np.array_equal(g.stream_counts(), g2.stream_counts())
+
+
+def test_partition_invariance_per_stream():
+    S = 256
+    for m in ("B1", "B2", "B3", "P"):
+        a, b = P.Generator(17, S), P.Generator(17, S)
+        one = gen_normals(a, m, 2 * S * 96, 0.0, 1.0).reshape(S, 192)
+        parts = [gen_normals(b, m, 2 * S * 32, 0.0, 1.0).reshape(S, 64) for _ in range(3)]
+        assert np.array_equal(one, np.concatenate(parts, axis=1))
+        assert np.array_equal(a.stream_counts(), b.stream_counts())
+
+
+def test_fake_shards_concatenate():
+    # multi-GPU partition emulated on one GPU: G handles over disjoint ranges
+    S, G, per = 1 << 12, 4, 2 * 40
+    full = gen_normals(P.Generator(11, S), "P", S * per, 0.0, 1.0)
+    parts = [gen_normals(P.Generator(11, S // G, first_stream=r * S // G), "P", S // G * per, 0.0, 1.0)
+             for r in range(G)]
+    assert np.array_equal(full, np.concatenate(parts))
+
+
+def test_checkpoint_resume():
+    S = 512
+    a = P.Generator(23, S)
+    a.normal("B1", 2 * S * 50)
+    ring, cnt = a.get_state()
+    x1 = gen_normals(a, "P", 2 * S * 70, 0.0, 1.0)
+    b = P.Generator(99, S)  # other seed, then restored
+    b.set_state(ring, cnt)
+    x2 = gen_normals(b, "P", 2 * S * 70, 0.0, 1.0)
+    assert np.array_equal(x1, x2)
+
+
+def test_above_2_32_outputs():
+    # 64-bit indexing: n = 2^32 + 6 over 2^16 streams; sample the first and last streams
+    S, n = 1 << 16, (1 << 32) + 6
+    free = torch.cuda.mem_get_info()[0]
+    if free < n * 8 + (2 << 30):
+        pytest.skip("not enough device memory")
+    g = P.Generator(5, S)
+    out = g.normal("B1", n)
+    pairs = (n + 1) // 2
+    q, rem = divmod(pairs, S)
+    for k in (0, rem - 1, rem, S - 1):
+        cnt = q + (k < rem)
+        off = 2 * (k * q + min(k, rem))
+        st = O.Streams(5, 1, first_stream=k)
+        o = st.normal_boxmuller(2 * cnt)
+        m = min(2 * cnt, n - off)
+        assert np.max(np.abs(host(out[off:off + m]) - o[:m])) <= TOL
+    del out
+
+
+# ---------------------------------------------------------------- validation reduction
+
+def test_stats_kernel_matches_oracle_stats():
+    c = W.C1
+    from scipy import stats as sps
+
+    K = 64
+    edges = c.mu + c.sigma * sps.norm.ppf(np.arange(1, K) / K)
+    g, st = P.Generator(c.seed, c.streams), O.Streams(c.seed, c.streams)
+    d = g.normal("B1", c.n, c.mu, c.sigma)
+    o = st.normal_boxmuller(c.n, c.mu, c.sigma, 1)
+    sums, hist = P.stats(d, c.mu, edges)
+    osums, ohist = O.stats(o, c.mu, edges)
+    sums, hist = host(sums), host(hist)
+    assert np.allclose(sums[:4], osums[:4], rtol=1e-9, atol=1e-9)
+    assert abs(sums[4] - osums[4]) <= TOL and abs(sums[5] - osums[5]) <= TOL
+    assert np.sum(np.abs(hist - ohist)) <= 2 and hist.sum() == c.n
+
+
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P"])
+def test_statistical_gates_at_c3_size(method):
+    from scipy import stats as sps
+
+    c = W.C3
+    g = P.Generator(c.seed + 1, c.streams)
+    x = g.normal(method, c.n, c.mu, c.sigma)
+    K = 256
+    edges = c.mu + c.sigma * sps.norm.ppf(np.arange(1, K) / K)
+    sums, hist = P.stats(x, c.mu, edges)
+    sums, hist = host(sums), host(hist)
+    n = c.n
+    m1 = sums[0] / n / c.sigma
+    m2 = sums[1] / n / c.sigma**2
+    assert abs(m1) < 4 / math.sqrt(n)
+    assert abs(m2 - 1) < 4 * math.sqrt(2 / n)
+    chi2 = np.sum((hist - n / K) ** 2 / (n / K))
+    assert chi2 < sps.chi2.ppf(0.999, K - 1)
