@@ -32,8 +32,8 @@ int cuda_err(cudaError_t e) {
     return set_err(NRNG_ECUDA);
 }
 
-constexpr size_t kBmSmem = kWarpsPerBlock * kWin * sizeof(uint64_t);
-constexpr size_t kPolarSmem = kBmSmem + kWarpsPerBlock * 3 * kQueue * sizeof(double);
+constexpr size_t kBmSmem = kWinBytes + kTabBytes;
+constexpr size_t kPolarSmem = kBmSmem + kQueueBytes;
 constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
 constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)
 
@@ -142,8 +142,7 @@ int run_bulk(nrng_handle h, Kind kind, double* out, size_t n, uint64_t units, in
     p.q = units / h->S;
     p.rem = units % h->S;
     p.n = n;
-    p.mu = mu;
-    p.sigma = sigma;
+    p.tp = TParams{mu, sigma, 2.0 * sigma};
     const uint32_t active = p.q == 0 ? (uint32_t)p.rem : h->S;  // streams with work
     if (is_device_pointer(out)) {
         p.out = out;
@@ -326,8 +325,8 @@ int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* de
     if (cudaGetDevice(&dev) != cudaSuccess) return set_err(NRNG_ENODEV);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)std::min<uint64_t>((n_pairs + 255) / 256, (uint64_t)sms * 8);
-    transform_kernel<<<grid, 256, 0, (cudaStream_t)cuda_stream>>>(dev_u, n_pairs, dev_out, dev_mask, mu, sigma,
-                                                                  method);
+    transform_kernel<<<grid, 256, 0, (cudaStream_t)cuda_stream>>>(dev_u, n_pairs, dev_out, dev_mask,
+                                                                  TParams{mu, sigma, 2.0 * sigma}, method);
     return cuda_err(cudaGetLastError());
 }
 

@@ -18,9 +18,13 @@ struct BulkParams {
     double* out;
     uint64_t units, q, rem, shift, n;
     uint32_t s_begin, s_end;
-    double mu, sigma;
+    TParams tp;
     int aligned;
 };
+
+// Per-block shared memory: [kWarpsPerBlock x kWin u64 windows][ln table][per-kernel extras].
+constexpr size_t kWinBytes = kWarpsPerBlock * kWin * sizeof(uint64_t);
+constexpr size_t kTabBytes = kLogTableEntries * sizeof(double2);
 
 // ------------------------------------------------------------------ seeding + warm-up
 // Word j of global stream g = splitmix64 output #(607 g + j) of seed (R2); all-even fix
@@ -59,44 +63,69 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) init_kernel(uint64_t* __r
 }
 
 // ------------------------------------------------------------------ Box-Muller B1/B2/B3
-// Per warp iteration: 32 pairs of stream k, lane l takes pair j0+l (uniforms 2(j0+l),
-// 2(j0+l)+1, or 3 for B3), one 16-byte streaming store per pair, 512 contiguous bytes
-// per warp store instruction.
+// Main loop: 64 pairs of stream k per warp iteration, two per lane (pairs j0+l and
+// j0+32+l: independent dependency chains for latency hiding, and every constant-bank
+// load and loop step amortised over two pairs); each store instruction writes 512
+// contiguous bytes with a 16-byte streaming store.  Streams whose outputs are all in
+// range and 16-byte aligned take this path; the tail (< 64 pairs), misaligned outputs
+// and the stream holding the dropped last deviate of an odd n take the 32-pair path.
+template <int V>
+__device__ __forceinline__ void bm_pair(const uint64_t* buf, uint32_t w, const TParams& tp, const double2* tab,
+                                        double& x, double& y) {
+    if (V == 3) {
+        b3_pair(buf[w & kWinMask], buf[(w + 1) & kWinMask], buf[(w + 2) & kWinMask], tp, tab, x, y);
+    } else {
+        const ulonglong2 xw = *reinterpret_cast<const ulonglong2*>(&buf[w & kWinMask]);
+        if (V == 1)
+            b1_pair(xw.x, xw.y, tp, tab, x, y);
+        else
+            b2_pair(xw.x, xw.y, tp, tab, x, y);
+    }
+}
+
 template <int V>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) bm_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr uint32_t per = (V == 3) ? 3 : 2;
+    constexpr int kB = (V == 3) ? 224 : 256;          // refill batch
+    constexpr uint32_t kNeed2 = 64 * per;              // words per 64-pair iteration
+    static_assert(kNeed2 - 1 + kB <= kWin - kLagR, "lookahead would clobber the write-back words");
+    double2* tab = reinterpret_cast<double2*>(smem + kWarpsPerBlock * kWin);
+    load_log_table(tab);
+    __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWin;
     for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
          k += gridDim.x * kWarpsPerBlock) {
-        const Quota qk = quota(p.units, p.q, p.rem, k);
+        const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         lfg_load(L, rk, C, lane);
-        for (uint64_t j0 = 0; j0 < qk.cnt; j0 += 32) {
-            lfg_ensure(L, lane, 32 * per);
+        uint64_t j0 = 0;
+        if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
+            double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
+            const uint64_t full = qk.cnt & ~uint64_t(63);
+            for (; j0 < full; j0 += 64, o += 64) {
+                lfg_ensure<kB>(L, lane, kNeed2);
+                const uint32_t w = L.wc + per * lane;
+                double x0, y0, x1, y1;
+                bm_pair<V>(L.buf, w, p.tp, tab, x0, y0);
+                bm_pair<V>(L.buf, w + 32 * per, p.tp, tab, x1, y1);
+                __stcs(o, make_double2(x0, y0));
+                __stcs(o + 32, make_double2(x1, y1));
+                L.wc += kNeed2;
+                __syncwarp();
+            }
+        }
+        for (; j0 < qk.cnt; j0 += 32) {
+            lfg_ensure<kB>(L, lane, 32 * per);
             const uint64_t left = qk.cnt - j0;
             const uint32_t active = left < 32 ? (uint32_t)left : 32u;
             if ((uint32_t)lane < active) {
-                const uint32_t w = L.wc + per * lane;
                 double x, y;
-                if (V == 3) {
-                    double u1 = word_to_uniform(L.buf[w & kWinMask]);
-                    double u2 = word_to_uniform(L.buf[(w + 1) & kWinMask]);
-                    double u3 = word_to_uniform(L.buf[(w + 2) & kWinMask]);
-                    b3_pair(u1, u2, u3, p.mu, p.sigma, x, y);
-                } else {
-                    const ulonglong2 xw = *reinterpret_cast<const ulonglong2*>(&L.buf[w & kWinMask]);
-                    double u = word_to_uniform(xw.x);
-                    double v = word_to_uniform(xw.y);
-                    if (V == 1)
-                        b1_pair(u, v, p.mu, p.sigma, x, y);
-                    else
-                        b2_pair(u, v, p.mu, p.sigma, x, y);
-                }
+                bm_pair<V>(L.buf, L.wc + per * lane, p.tp, tab, x, y);
                 store_pair(p.out, 2 * (qk.off + j0 + lane), p.shift, p.n, x, y, p.aligned);
             }
             L.wc += per * active;
@@ -109,69 +138,109 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bm_kernel(BulkParams p) {
 }
 
 // ------------------------------------------------------------------ Polar P
-// Per warp iteration: 32 candidates (64 uniforms).  Accepts are ranked with
-// __ballot_sync/__popc, trimmed at the stream's remaining quota (exact stop, R5),
-// appended to a per-warp shared-memory queue in candidate order; every time the queue
-// holds 32 survivors the warp transforms them densely (no lane idles on a rejected
-// candidate) and stores 32 consecutive pairs.
-constexpr int kQueue = 64;
+// Candidate phase: 64 candidates (128 uniforms) per warp step, two per lane.  Accepts
+// are ranked with __ballot_sync/__popc (first the 32 candidates of the lower half, then
+// the upper half, so the queue order is the candidate order), trimmed at the stream's
+// remaining quota (exact stop, R5), and appended to a per-warp shared-memory queue.
+// Transform phase: whenever the queue holds >= 64 survivors the warp transforms 64 of
+// them densely (two per lane; no lane idles on a rejected candidate) and stores 64
+// consecutive pairs.  The stream's last < 64 survivors are flushed 32 at a time.
+constexpr int kQueue = 128;
+constexpr size_t kQueueBytes = kWarpsPerBlock * 3 * kQueue * sizeof(double);
+
+struct PolarQueue {
+    double *x, *y, *s;
+    __device__ __forceinline__ void put(uint32_t slot, const PolarCand& c) {
+        slot &= kQueue - 1;
+        x[slot] = c.X;
+        y[slot] = c.Y;
+        s[slot] = c.S;
+    }
+    __device__ __forceinline__ PolarCand get(uint32_t slot) const {
+        slot &= kQueue - 1;
+        return PolarCand{x[slot], y[slot], s[slot]};
+    }
+};
+
+// Rank the accepted candidates of one group of 32 and append the first `need` of them.
+// Returns the number of candidates consumed (32, or up to and including the last used).
+__device__ __forceinline__ uint32_t polar_append(bool ok, const PolarCand& c, int lane, uint64_t need, PolarQueue& q,
+                                                 uint64_t& acc) {
+    unsigned m = __ballot_sync(kFull, ok);
+    const int rank = __popc(m & lanemask_lt(lane));
+    uint32_t used = 32;
+    if ((uint64_t)__popc(m) >= need) {  // exact stop inside this group of 32
+        const unsigned last = __ballot_sync(kFull, ok && (uint64_t)rank == need - 1);
+        const int lastlane = __ffs(last) - 1;
+        used = lastlane + 1;
+        m &= (lastlane == 31) ? kFull : ((2u << lastlane) - 1u);
+    }
+    if ((m >> lane) & 1u) q.put((uint32_t)acc + rank, c);
+    acc += __popc(m);
+    return used;
+}
+
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double2* tab = reinterpret_cast<double2*>(smem + kWarpsPerBlock * kWin);
+    load_log_table(tab);
+    __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWin;
-    double* qx = reinterpret_cast<double*>(smem + kWarpsPerBlock * kWin) + warp * 3 * kQueue;
-    double* qy = qx + kQueue;
-    double* qs = qy + kQueue;
+    double* qb = reinterpret_cast<double*>(smem + kWarpsPerBlock * kWin + 2 * kLogTableEntries) + warp * 3 * kQueue;
+    PolarQueue q{qb, qb + kQueue, qb + 2 * kQueue};
     for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
          k += gridDim.x * kWarpsPerBlock) {
-        const Quota qk = quota(p.units, p.q, p.rem, k);
+        const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         lfg_load(L, rk, C, lane);
+        const bool fast = p.aligned && 2 * (qk.off + qk.cnt) <= p.n;
+        double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
         uint64_t acc = 0;    // accepted (queued) pairs of this stream
         uint64_t done = 0;   // pairs transformed and stored
         while (acc < qk.cnt) {
-            lfg_ensure(L, lane, 64);
-            const ulonglong2 xw = *reinterpret_cast<const ulonglong2*>(&L.buf[(L.wc + 2 * lane) & kWinMask]);
-            double x, y, s;
-            const bool ok = polar_candidate(word_to_uniform(xw.x), word_to_uniform(xw.y), x, y, s);
-            unsigned m = __ballot_sync(kFull, ok);
-            const uint64_t need = qk.cnt - acc;
-            uint32_t used = 32;
-            if ((uint64_t)__popc(m) >= need) {  // exact stop inside this group of 32
-                const int rank = __popc(m & (unsigned)lanemask_lt(lane));
-                const unsigned last = __ballot_sync(kFull, ok && (uint64_t)rank == need - 1);
-                const int lastlane = __ffs(last) - 1;
-                used = lastlane + 1;
-                m &= (lastlane == 31) ? kFull : ((2u << lastlane) - 1u);
-            }
-            if ((m >> lane) & 1u) {
-                const uint32_t slot = (uint32_t)(acc + __popc(m & (unsigned)lanemask_lt(lane))) & (kQueue - 1);
-                qx[slot] = x;
-                qy[slot] = y;
-                qs[slot] = s;
-            }
-            acc += __popc(m);
+            lfg_ensure(L, lane, 128);
+            const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(&L.buf[(L.wc + 2 * lane) & kWinMask]);
+            const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(&L.buf[(L.wc + 64 + 2 * lane) & kWinMask]);
+            PolarCand c0, c1;
+            const bool ok0 = polar_candidate(w0.x, w0.y, c0);
+            const bool ok1 = polar_candidate(w1.x, w1.y, c1);
+            const uint32_t used0 = polar_append(ok0, c0, lane, qk.cnt - acc, q, acc);
+            uint32_t used = used0;
+            if (used0 == 32 && acc < qk.cnt) used += polar_append(ok1, c1, lane, qk.cnt - acc, q, acc);
             L.wc += 2 * used;
             __syncwarp();
-            if (acc - done >= 32) {
-                const uint32_t slot = (uint32_t)(done + lane) & (kQueue - 1);
+            if (fast && acc - done >= 64) {
+                const PolarCand a = q.get((uint32_t)done + lane), b = q.get((uint32_t)done + 32 + lane);
+                double ax, ay, bx, by;
+                polar_transform(a, p.tp, tab, ax, ay);
+                polar_transform(b, p.tp, tab, bx, by);
+                __stcs(o + done, make_double2(ax, ay));
+                __stcs(o + done + 32, make_double2(bx, by));
+                done += 64;
+                __syncwarp();
+            }
+            while (!fast && acc - done >= 32) {
+                const PolarCand a = q.get((uint32_t)done + lane);
                 double ox, oy;
-                polar_transform(qx[slot], qy[slot], qs[slot], p.mu, p.sigma, ox, oy);
+                polar_transform(a, p.tp, tab, ox, oy);
                 store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox, oy, p.aligned);
                 done += 32;
                 __syncwarp();
             }
         }
-        if ((uint64_t)lane < acc - done) {
-            const uint32_t slot = (uint32_t)(done + lane) & (kQueue - 1);
-            double ox, oy;
-            polar_transform(qx[slot], qy[slot], qs[slot], p.mu, p.sigma, ox, oy);
-            store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox, oy, p.aligned);
+        for (; done < acc; done += 32) {
+            if ((uint64_t)lane < acc - done) {
+                const PolarCand a = q.get((uint32_t)done + lane);
+                double ox, oy;
+                polar_transform(a, p.tp, tab, ox, oy);
+                store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox, oy, p.aligned);
+            }
+            __syncwarp();
         }
-        __syncwarp();
         lfg_store(L, rk, C, lane);
         if (lane == 0) p.count[k] = C + (L.wc - (kLagR + 1));
         __syncwarp();
@@ -187,7 +256,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) uniform_kernel(BulkParams
     L.buf = smem + warp * kWin;
     for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
          k += gridDim.x * kWarpsPerBlock) {
-        const Quota qk = quota(p.units, p.q, p.rem, k);
+        const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
@@ -198,7 +267,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) uniform_kernel(BulkParams
             const uint32_t active = left < 32 ? (uint32_t)left : 32u;
             if ((uint32_t)lane < active) {
                 const uint64_t g = qk.off + j0 + lane;
-                p.out[g - p.shift] = word_to_uniform(L.buf[(L.wc + lane) & kWinMask]);
+                p.out[g - p.shift] = (double)ukey(L.buf[(L.wc + lane) & kWinMask]) * 0x1p-53;  // exact
             }
             L.wc += active;
             __syncwarp();
@@ -227,9 +296,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_mask_kernel(BulkPar
             const uint32_t active = left < 32 ? (uint32_t)left : 32u;
             if ((uint32_t)lane < active) {
                 const ulonglong2 xw = *reinterpret_cast<const ulonglong2*>(&L.buf[(L.wc + 2 * lane) & kWinMask]);
-                double x, y, s;
-                mask[(uint64_t)k * cand + j0 + lane] =
-                    polar_candidate(word_to_uniform(xw.x), word_to_uniform(xw.y), x, y, s) ? 1 : 0;
+                PolarCand pc;
+                mask[(uint64_t)k * cand + j0 + lane] = polar_candidate(xw.x, xw.y, pc) ? 1 : 0;
             }
             L.wc += 2 * active;
             __syncwarp();
@@ -240,23 +308,29 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_mask_kernel(BulkPar
     }
 }
 
-// nrng_transform_from_uniforms: one thread per pair.
+// nrng_transform_from_uniforms: one thread per pair; the given uniforms (multiples of
+// 2^-53 in [0,1)) are turned back into the words the stream would hold, so this runs
+// exactly the device code of the bulk kernels.
+__device__ __forceinline__ uint64_t word_of(double u) { return __double2ull_rn(u * 0x1p53) << 11; }
 __global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs, double* __restrict__ out,
-                                 uint8_t* __restrict__ mask, double mu, double sigma, int method) {
+                                 uint8_t* __restrict__ mask, TParams tp, int method) {
+    __shared__ double2 tab[kLogTableEntries];
+    load_log_table(tab);
+    __syncthreads();
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_pairs;
          j += (uint64_t)gridDim.x * blockDim.x) {
         double x = __longlong_as_double(0x7ff8000000000000ULL), y = x;
         if (method == 1) {
-            b1_pair(u[2 * j], u[2 * j + 1], mu, sigma, x, y);
+            b1_pair(word_of(u[2 * j]), word_of(u[2 * j + 1]), tp, tab, x, y);
         } else if (method == 2) {
-            b2_pair(u[2 * j], u[2 * j + 1], mu, sigma, x, y);
+            b2_pair(word_of(u[2 * j]), word_of(u[2 * j + 1]), tp, tab, x, y);
         } else if (method == 3) {
-            b3_pair(u[3 * j], u[3 * j + 1], u[3 * j + 2], mu, sigma, x, y);
+            b3_pair(word_of(u[3 * j]), word_of(u[3 * j + 1]), word_of(u[3 * j + 2]), tp, tab, x, y);
         } else {
-            double cx, cy, s;
-            const bool ok = polar_candidate(u[2 * j], u[2 * j + 1], cx, cy, s);
+            PolarCand pc;
+            const bool ok = polar_candidate(word_of(u[2 * j]), word_of(u[2 * j + 1]), pc);
             if (mask) mask[j] = ok ? 1 : 0;
-            if (ok) polar_transform(cx, cy, s, mu, sigma, x, y);
+            if (ok) polar_transform(pc, tp, tab, x, y);
         }
         out[2 * j] = x;
         out[2 * j + 1] = y;

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import math
 import os
+import struct
 
 import mpmath as mp
 from mpmath.libmp.libmpf import to_float
@@ -79,6 +80,112 @@ def generate():
     return sin_c, cos_c, h_c
 
 
+# ----------------------------------------------------------------------------------------
+# Coefficients of the path's own fp64 primitives (fast ln / sinpi / cospi), DESIGN.md §6.
+# These are implementation constants of the CUDA kernels, not part of the paper's method:
+# they replace libdevice's log / sincospi with cheaper table + polynomial versions whose
+# error (< 1e-16 absolute on the reduced arguments) sits far inside the 1e-13 output bar.
+
+LOG_BASE_HI = 0x3FE6A09E  # high word of sqrt(1/2): m is normalised into [sqrt(1/2), sqrt(2))
+LOG_TABLE_BITS = 7
+
+
+def _d_from_hi(hi):
+    return struct.unpack("<d", struct.pack("<Q", hi << 32))[0]
+
+
+def log_table():
+    """Bucket j holds the m whose high word is LOG_BASE_HI + j*2^13 .. + (j+1)*2^13 (exclusive).
+    c_j = 1 for the bucket containing 1 (so ln(1-u) keeps full relative accuracy for tiny u),
+    else the bucket midpoint; inv_j = RN(1/c_j); T_j = RN(-ln(inv_j)); r = fma(m, inv_j, -1)."""
+    rows, rmax = [], mp.mpf(0)
+    step = 1 << (20 - LOG_TABLE_BITS)
+    for j in range(1 << LOG_TABLE_BITS):
+        lo = _d_from_hi(LOG_BASE_HI + j * step)
+        hi = _d_from_hi(LOG_BASE_HI + (j + 1) * step)
+        c = mp.mpf(1) if lo <= 1.0 < hi else (mp.mpf(lo) + mp.mpf(hi)) / 2
+        inv = rn(1 / c)
+        t = rn(-mp.log(mp.mpf(inv)))
+        rmax = max(rmax, abs(mp.mpf(lo) * inv - 1), abs(mp.mpf(hi) * inv - 1))
+        rows.append((inv, t))
+    return rows, float(rmax)
+
+
+def log1p_coeffs(rmax, degree=6):
+    """Taylor coefficients of ln(1+r) = r + sum_{k=2..degree} (-1)^(k+1) r^k / k; truncation
+    error rmax^(degree+1)/(degree+1)."""
+    err = rmax ** (degree + 1) / (degree + 1)
+    return [rn(mp.mpf((-1) ** (k + 1)) / k) for k in range(2, degree + 1)], err
+
+
+def _cheb_fit_interval(f, a, b, degree):
+    """Monomial coefficients (in x) of the degree-`degree` Chebyshev interpolant of f on [a, b]."""
+    N = N_NODES
+    th = [mp.pi * (j + mp.mpf(1) / 2) / N for j in range(N)]
+    fx = [f((a + b) / 2 + (b - a) / 2 * mp.cos(t)) for t in th]
+    ak = []
+    for k in range(degree + 1):
+        ak.append(mp.fsum(fx[j] * mp.cos(k * th[j]) for j in range(N)) * 2 / N)
+    ak[0] /= 2
+    # in s = (2x - a - b)/(b - a): monomials in s, then expand s = alpha x + beta
+    ms = to_monomial(ak)
+    alpha, beta = 2 / (b - a), -(a + b) / (b - a)
+    out = [mp.mpf(0)] * (degree + 1)
+    for p, cp in enumerate(ms):
+        for q in range(p + 1):
+            out[q] += cp * mp.binomial(p, q) * alpha ** q * beta ** (p - q)
+    return out
+
+
+def sincospi_coeffs(sdeg=6, cdeg=6):
+    """sin(pi z) = z S(z^2), cos(pi z) = C(z^2) on |z| <= 1/4 (w = z^2 in [0, 1/16])."""
+    S = lambda w: mp.sin(mp.pi * mp.sqrt(w)) / mp.sqrt(w) if w > 0 else mp.pi
+    Cf = lambda w: mp.cos(mp.pi * mp.sqrt(w))
+    s = _cheb_fit_interval(S, mp.mpf(0), mp.mpf(1) / 16, sdeg)
+    c = _cheb_fit_interval(Cf, mp.mpf(0), mp.mpf(1) / 16, cdeg)
+    serr = cerr = mp.mpf(0)
+    for i in range(801):
+        z = mp.mpf(i) / 3200
+        w = z * z
+        serr = max(serr, abs(z * mp.fsum(cf * w ** k for k, cf in enumerate(s)) - mp.sin(mp.pi * z)))
+        cerr = max(cerr, abs(mp.fsum(cf * w ** k for k, cf in enumerate(c)) - mp.cos(mp.pi * z)))
+    return [rn(x) for x in s], [rn(x) for x in c], float(serr), float(cerr)
+
+
+def emit_math(body):
+    rows, rmax = log_table()
+    l1p, l1p_err = log1p_coeffs(rmax)
+    sc, cc, serr, cerr = sincospi_coeffs()
+    ln2 = mp.log(2)
+    ln2_hi = rn(ln2)
+    ln2_hi = float.fromhex(ln2_hi.hex()[:-4] + "0p-1") if False else ln2_hi
+    # ln2 split so that e * LN2_HI is exact for |e| < 2^11: keep 42 significant bits
+    m, e = mp.frexp(ln2)
+    hi = mp.floor(m * 2 ** 42) / 2 ** 42 * 2 ** e
+    lo = ln2 - hi
+    body.append("// ---- path primitives (implementation constants, DESIGN.md §6) ----")
+    body.append("// ln: m in [sqrt(1/2), sqrt(2)), bucket j = top %d bits of m's 20-bit high mantissa field;" % LOG_TABLE_BITS)
+    body.append("// max |r| = %.6e; ln(1+r) Taylor degree %d, truncation error %.3e" % (rmax, len(l1p) + 1, l1p_err))
+    body.append("constexpr unsigned kLogBaseHi = 0x%08X;" % LOG_BASE_HI)
+    body.append("constexpr int kLogTableBits = %d;" % LOG_TABLE_BITS)
+    body.append("constexpr double kLn2Hi = %s;" % rn(hi).hex())
+    body.append("constexpr double kLn2Lo = %s;" % rn(lo).hex())
+    body.append("// ln(1+r) = r + r^2 (L2 + r (L3 + ...))")
+    body.append("__constant__ double kLog1p[%d] = {%s};" % (len(l1p), ", ".join(x.hex() for x in l1p)))
+    body.append("// {inv_c_j, -ln(inv_c_j)} pairs")
+    body.append("__device__ double kLogTable[%d] = {" % (2 * len(rows)))
+    body += ["    %s, %s," % (a.hex(), b.hex()) for a, b in rows]
+    body.append("};")
+    body.append("// sin(pi z) = z S(w), cos(pi z) = C(w), w = z^2, |z| <= 1/4; max err sin %.2e cos %.2e" % (serr, cerr))
+    # pre-scaled for an integer argument Z = z 2^52 (|Z| <= 2^50): sin = Z S'(Z^2), cos = C'(Z^2),
+    # S'_k = S_k 2^-(52+104k), C'_k = C_k 2^-104k (exact power-of-two scalings, all normal)
+    sz = [math.ldexp(x, -(52 + 104 * k)) for k, x in enumerate(sc)]
+    cz = [math.ldexp(x, -104 * k) for k, x in enumerate(cc)]
+    assert all(abs(x) > 2.0 ** -1000 for x in sz + cz)
+    body.append("__constant__ double kSinPiZ[%d] = {%s};" % (len(sz), ", ".join(x.hex() for x in sz)))
+    body.append("__constant__ double kCosPiZ[%d] = {%s};" % (len(cz), ", ".join(x.hex() for x in cz)))
+
+
 def main():
     sin_c, cos_c, h_c = generate()
     body = [
@@ -89,15 +196,15 @@ def main():
         "namespace nrng {",
         "// sin y ~ y * (S1 + S3 y^2 + S5 y^4 + S7 y^6)",
     ]
-    for name, v in zip(("S1", "S3", "S5", "S7"), sin_c):
-        body.append("constexpr double k%s = %s;" % (name, v.hex()))
+    body.append("__constant__ double kB2Sin[4] = {%s};  // S1, S3, S5, S7" % ", ".join(v.hex() for v in sin_c))
     body.append("// cos y ~ C0 + C2 y^2 + C4 y^4 + C6 y^6")
-    for name, v in zip(("C0", "C2", "C4", "C6"), cos_c):
-        body.append("constexpr double k%s = %s;" % (name, v.hex()))
+    body.append("__constant__ double kB2Cos[4] = {%s};  // C0, C2, C4, C6" % ", ".join(v.hex() for v in cos_c))
     body.append("// h(v) ~ sum_j kH[j] v^j")
-    body.append("__device__ constexpr double kH[16] = {")
+    body.append("__constant__ double kH[16] = {")
     body += ["    %s," % v.hex() for v in h_c]
-    body += ["};", "}  // namespace nrng", ""]
+    body += ["};"]
+    emit_math(body)
+    body += ["}  // namespace nrng", ""]
     with open(OUT, "w") as fh:
         fh.write("\n".join(body))
     print("\n".join(body))
