@@ -23,7 +23,7 @@ struct BulkParams {
 };
 
 // Per-block shared memory: [kWarpsPerBlock x kWin u64 windows][ln table][per-kernel extras].
-constexpr size_t kWinBytes = kWarpsPerBlock * kWin * sizeof(uint64_t);
+constexpr size_t kWinBytes = kWarpsPerBlock * kWinAlloc * sizeof(uint64_t);
 constexpr size_t kTabBytes = kLogTableEntries * sizeof(double2);
 
 // ------------------------------------------------------------------ seeding + warm-up
@@ -69,33 +69,50 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) init_kernel(uint64_t* __r
 // contiguous bytes with a 16-byte streaming store.  Streams whose outputs are all in
 // range and 16-byte aligned take this path; the tail (< 64 pairs), misaligned outputs
 // and the stream holding the dropped last deviate of an odd n take the 32-pair path.
-template <int V>
-__device__ __forceinline__ void bm_pair(const uint64_t* buf, uint32_t w, const TParams& tp, const double2* tab,
-                                        double& x, double& y) {
+// U pairs per lane: pair u reads its words at src + u * 32 * per (lane-interleaved).
+template <int V, int U>
+__device__ __forceinline__ void bm_pairs(const uint64_t* src, const TParams& tp, const double2* tab, double (&x)[U],
+                                         double (&y)[U]) {
+    constexpr int per = (V == 3) ? 3 : 2;
     if (V == 3) {
-        b3_pair(buf[w & kWinMask], buf[(w + 1) & kWinMask], buf[(w + 2) & kWinMask], tp, tab, x, y);
+        uint64_t w1[U], w2[U], w3[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            w1[u] = src[32 * per * u];
+            w2[u] = src[32 * per * u + 1];
+            w3[u] = src[32 * per * u + 2];
+        }
+        b3_pairs<U>(w1, w2, w3, tp, tab, x, y);
     } else {
-        const ulonglong2 xw = *reinterpret_cast<const ulonglong2*>(&buf[w & kWinMask]);
+        uint64_t wu[U], wv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const ulonglong2 xw = *reinterpret_cast<const ulonglong2*>(src + 32 * per * u);
+            wu[u] = xw.x;
+            wv[u] = xw.y;
+        }
         if (V == 1)
-            b1_pair(xw.x, xw.y, tp, tab, x, y);
+            b1_pairs<U>(wu, wv, tp, tab, x, y);
         else
-            b2_pair(xw.x, xw.y, tp, tab, x, y);
+            b2_pairs<U>(wu, wv, tp, tab, x, y);
     }
 }
 
 template <int V>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) bm_kernel(BulkParams p) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 5) bm_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr uint32_t per = (V == 3) ? 3 : 2;
-    constexpr int kB = (V == 3) ? 224 : 256;          // refill batch
-    constexpr uint32_t kNeed2 = 64 * per;              // words per 64-pair iteration
-    static_assert(kNeed2 - 1 + kB <= kWin - kLagR, "lookahead would clobber the write-back words");
-    double2* tab = reinterpret_cast<double2*>(smem + kWarpsPerBlock * kWin);
+    constexpr int kU = (V == 3) ? 2 : 4;               // pairs per lane per main-loop iteration
+    constexpr int kB = 128;                            // refill batch
+    constexpr uint32_t kNeedU = 32 * kU * per;         // words per main-loop iteration
+    static_assert(kNeedU - 1 + kB <= kWin - kLagR, "lookahead would clobber the write-back words");
+    static_assert(kNeedU <= kMirror, "unmasked reads must stay inside the mirror");
+    double2* tab = reinterpret_cast<double2*>(smem + kWarpsPerBlock * kWinAlloc);
     load_log_table(tab);
     __syncthreads();
     WarpLFG L;
-    L.buf = smem + warp * kWin;
+    L.buf = smem + warp * kWinAlloc;
     for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
          k += gridDim.x * kWarpsPerBlock) {
         const Quota qk = quota(p.q, p.rem, k);
@@ -106,16 +123,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bm_kernel(BulkParams p) {
         uint64_t j0 = 0;
         if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
             double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
-            const uint64_t full = qk.cnt & ~uint64_t(63);
-            for (; j0 < full; j0 += 64, o += 64) {
-                lfg_ensure<kB>(L, lane, kNeed2);
-                const uint32_t w = L.wc + per * lane;
-                double x0, y0, x1, y1;
-                bm_pair<V>(L.buf, w, p.tp, tab, x0, y0);
-                bm_pair<V>(L.buf, w + 32 * per, p.tp, tab, x1, y1);
-                __stcs(o, make_double2(x0, y0));
-                __stcs(o + 32, make_double2(x1, y1));
-                L.wc += kNeed2;
+            const uint64_t full = qk.cnt - qk.cnt % (32 * kU);
+            for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
+                lfg_ensure<kB>(L, lane, kNeedU);
+                const uint64_t* src = L.at(per * lane);
+                double x[kU], y[kU];
+                bm_pairs<V, kU>(src, p.tp, tab, x, y);
+#pragma unroll
+                for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+                L.wc += kNeedU;
                 __syncwarp();
             }
         }
@@ -124,15 +140,15 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) bm_kernel(BulkParams p) {
             const uint64_t left = qk.cnt - j0;
             const uint32_t active = left < 32 ? (uint32_t)left : 32u;
             if ((uint32_t)lane < active) {
-                double x, y;
-                bm_pair<V>(L.buf, L.wc + per * lane, p.tp, tab, x, y);
-                store_pair(p.out, 2 * (qk.off + j0 + lane), p.shift, p.n, x, y, p.aligned);
+                double x[1], y[1];
+                bm_pairs<V, 1>(L.at(per * lane), p.tp, tab, x, y);
+                store_pair(p.out, 2 * (qk.off + j0 + lane), p.shift, p.n, x[0], y[0], p.aligned);
             }
             L.wc += per * active;
             __syncwarp();
         }
         lfg_store(L, rk, C, lane);
-        if (lane == 0) p.count[k] = C + (L.wc - (kLagR + 1));
+        if (lane == 0) p.count[k] = C + (L.wc - kW0);
         __syncwarp();
     }
 }
@@ -180,15 +196,15 @@ __device__ __forceinline__ uint32_t polar_append(bool ok, const PolarCand& c, in
     return used;
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_kernel(BulkParams p) {
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) polar_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double2* tab = reinterpret_cast<double2*>(smem + kWarpsPerBlock * kWin);
+    double2* tab = reinterpret_cast<double2*>(smem + kWarpsPerBlock * kWinAlloc);
     load_log_table(tab);
     __syncthreads();
     WarpLFG L;
-    L.buf = smem + warp * kWin;
-    double* qb = reinterpret_cast<double*>(smem + kWarpsPerBlock * kWin + 2 * kLogTableEntries) + warp * 3 * kQueue;
+    L.buf = smem + warp * kWinAlloc;
+    double* qb = reinterpret_cast<double*>(smem + kWarpsPerBlock * kWinAlloc + 2 * kLogTableEntries) + warp * 3 * kQueue;
     PolarQueue q{qb, qb + kQueue, qb + 2 * kQueue};
     for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
          k += gridDim.x * kWarpsPerBlock) {
@@ -203,8 +219,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_kernel(BulkParams p
         uint64_t done = 0;   // pairs transformed and stored
         while (acc < qk.cnt) {
             lfg_ensure(L, lane, 128);
-            const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(&L.buf[(L.wc + 2 * lane) & kWinMask]);
-            const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(&L.buf[(L.wc + 64 + 2 * lane) & kWinMask]);
+            const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(L.at(2 * lane));
+            const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(L.at(64 + 2 * lane));
             PolarCand c0, c1;
             const bool ok0 = polar_candidate(w0.x, w0.y, c0);
             const bool ok1 = polar_candidate(w1.x, w1.y, c1);
@@ -214,35 +230,34 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_kernel(BulkParams p
             L.wc += 2 * used;
             __syncwarp();
             if (fast && acc - done >= 64) {
-                const PolarCand a = q.get((uint32_t)done + lane), b = q.get((uint32_t)done + 32 + lane);
-                double ax, ay, bx, by;
-                polar_transform(a, p.tp, tab, ax, ay);
-                polar_transform(b, p.tp, tab, bx, by);
-                __stcs(o + done, make_double2(ax, ay));
-                __stcs(o + done + 32, make_double2(bx, by));
+                const PolarCand c[2] = {q.get((uint32_t)done + lane), q.get((uint32_t)done + 32 + lane)};
+                double ox[2], oy[2];
+                polar_transform<2>(c, p.tp, tab, ox, oy);
+                __stcs(o + done, make_double2(ox[0], oy[0]));
+                __stcs(o + done + 32, make_double2(ox[1], oy[1]));
                 done += 64;
                 __syncwarp();
             }
             while (!fast && acc - done >= 32) {
-                const PolarCand a = q.get((uint32_t)done + lane);
-                double ox, oy;
-                polar_transform(a, p.tp, tab, ox, oy);
-                store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox, oy, p.aligned);
+                const PolarCand c[1] = {q.get((uint32_t)done + lane)};
+                double ox[1], oy[1];
+                polar_transform<1>(c, p.tp, tab, ox, oy);
+                store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
                 done += 32;
                 __syncwarp();
             }
         }
         for (; done < acc; done += 32) {
             if ((uint64_t)lane < acc - done) {
-                const PolarCand a = q.get((uint32_t)done + lane);
-                double ox, oy;
-                polar_transform(a, p.tp, tab, ox, oy);
-                store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox, oy, p.aligned);
+                const PolarCand c[1] = {q.get((uint32_t)done + lane)};
+                double ox[1], oy[1];
+                polar_transform<1>(c, p.tp, tab, ox, oy);
+                store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
             }
             __syncwarp();
         }
         lfg_store(L, rk, C, lane);
-        if (lane == 0) p.count[k] = C + (L.wc - (kLagR + 1));
+        if (lane == 0) p.count[k] = C + (L.wc - kW0);
         __syncwarp();
     }
 }
@@ -253,7 +268,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) uniform_kernel(BulkParams
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpLFG L;
-    L.buf = smem + warp * kWin;
+    L.buf = smem + warp * kWinAlloc;
     for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
          k += gridDim.x * kWarpsPerBlock) {
         const Quota qk = quota(p.q, p.rem, k);
@@ -273,7 +288,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) uniform_kernel(BulkParams
             __syncwarp();
         }
         lfg_store(L, rk, C, lane);
-        if (lane == 0) p.count[k] = C + (L.wc - (kLagR + 1));
+        if (lane == 0) p.count[k] = C + (L.wc - kW0);
         __syncwarp();
     }
 }
@@ -284,7 +299,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_mask_kernel(BulkPar
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpLFG L;
-    L.buf = smem + warp * kWin;
+    L.buf = smem + warp * kWinAlloc;
     for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
          k += gridDim.x * kWarpsPerBlock) {
         const uint64_t C = p.count[k];
@@ -303,7 +318,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_mask_kernel(BulkPar
             __syncwarp();
         }
         lfg_store(L, rk, C, lane);
-        if (lane == 0) p.count[k] = C + (L.wc - (kLagR + 1));
+        if (lane == 0) p.count[k] = C + (L.wc - kW0);
         __syncwarp();
     }
 }
@@ -319,21 +334,24 @@ __global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs,
     __syncthreads();
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_pairs;
          j += (uint64_t)gridDim.x * blockDim.x) {
-        double x = __longlong_as_double(0x7ff8000000000000ULL), y = x;
-        if (method == 1) {
-            b1_pair(word_of(u[2 * j]), word_of(u[2 * j + 1]), tp, tab, x, y);
-        } else if (method == 2) {
-            b2_pair(word_of(u[2 * j]), word_of(u[2 * j + 1]), tp, tab, x, y);
+        double x[1] = {__longlong_as_double(0x7ff8000000000000ULL)}, y[1] = {x[0]};
+        if (method == 1 || method == 2) {
+            const uint64_t wu[1] = {word_of(u[2 * j])}, wv[1] = {word_of(u[2 * j + 1])};
+            if (method == 1)
+                b1_pairs<1>(wu, wv, tp, tab, x, y);
+            else
+                b2_pairs<1>(wu, wv, tp, tab, x, y);
         } else if (method == 3) {
-            b3_pair(word_of(u[3 * j]), word_of(u[3 * j + 1]), word_of(u[3 * j + 2]), tp, tab, x, y);
+            const uint64_t w1[1] = {word_of(u[3 * j])}, w2[1] = {word_of(u[3 * j + 1])}, w3[1] = {word_of(u[3 * j + 2])};
+            b3_pairs<1>(w1, w2, w3, tp, tab, x, y);
         } else {
-            PolarCand pc;
-            const bool ok = polar_candidate(word_of(u[2 * j]), word_of(u[2 * j + 1]), pc);
+            PolarCand pc[1];
+            const bool ok = polar_candidate(word_of(u[2 * j]), word_of(u[2 * j + 1]), pc[0]);
             if (mask) mask[j] = ok ? 1 : 0;
-            if (ok) polar_transform(pc, tp, tab, x, y);
+            if (ok) polar_transform<1>(pc, tp, tab, x, y);
         }
-        out[2 * j] = x;
-        out[2 * j + 1] = y;
+        out[2 * j] = x[0];
+        out[2 * j + 1] = y[0];
     }
 }
 

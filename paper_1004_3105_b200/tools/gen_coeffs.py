@@ -177,10 +177,10 @@ def emit_math(body):
     body += ["    %s, %s," % (a.hex(), b.hex()) for a, b in rows]
     body.append("};")
     body.append("// sin(pi z) = z S(w), cos(pi z) = C(w), w = z^2, |z| <= 1/4; max err sin %.2e cos %.2e" % (serr, cerr))
-    # pre-scaled for an integer argument Z = z 2^52 (|Z| <= 2^50): sin = Z S'(Z^2), cos = C'(Z^2),
-    # S'_k = S_k 2^-(52+104k), C'_k = C_k 2^-104k (exact power-of-two scalings, all normal)
-    sz = [math.ldexp(x, -(52 + 104 * k)) for k, x in enumerate(sc)]
-    cz = [math.ldexp(x, -104 * k) for k, x in enumerate(cc)]
+    # pre-scaled for an integer argument Z = z 2^63 (|Z| <= 2^61): sin = Z S'(Z^2), cos = C'(Z^2),
+    # S'_k = S_k 2^-(63+126k), C'_k = C_k 2^-126k (exact power-of-two scalings, all normal)
+    sz = [math.ldexp(x, -(63 + 126 * k)) for k, x in enumerate(sc)]
+    cz = [math.ldexp(x, -126 * k) for k, x in enumerate(cc)]
     assert all(abs(x) > 2.0 ** -1000 for x in sz + cz)
     body.append("__constant__ double kSinPiZ[%d] = {%s};" % (len(sz), ", ".join(x.hex() for x in sz)))
     body.append("__constant__ double kCosPiZ[%d] = {%s};" % (len(cz), ", ".join(x.hex() for x in cz)))
