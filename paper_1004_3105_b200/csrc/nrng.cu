@@ -32,13 +32,14 @@ int cuda_err(cudaError_t e) {
     return set_err(NRNG_ECUDA);
 }
 
-constexpr size_t kBmSmem = kWinBytes + kTabBytes;
-constexpr size_t kPolarSmem = kBmSmem + kQueueBytes;
+constexpr size_t bm_smem(int nw) { return win_bytes(nw) + kTabBytes; }
+constexpr size_t polar_smem(int nw) { return bm_smem(nw) + queue_bytes(nw); }
+constexpr size_t kUniSmem = win_bytes(kWarpsPerBlock);
 constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
 constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)
 
 struct Occ {
-    int bm1 = 0, bm2 = 0, bm3 = 0, polar = 0, uni = 0, mask = 0, init = 0;
+    int bm[4] = {0, 0, 0, 0}, polar = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
 };
 
 }  // namespace
@@ -63,11 +64,11 @@ struct nrng_gen {
 namespace {
 
 template <typename K>
-int occupancy(K kernel, size_t smem) {
+int occupancy(K kernel, int nw, size_t smem) {
     int b = 0;
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kWarpsPerBlock * 32, smem) != cudaSuccess) b = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, nw * 32, smem) != cudaSuccess) b = 1;
     return std::max(b, 1);
 }
 
@@ -77,32 +78,43 @@ bool check_device(nrng_handle h) {
     return d == h->device;
 }
 
-unsigned grid_for(uint32_t nstreams, int per_sm, int num_sms) {
-    uint64_t want = (nstreams + kWarpsPerBlock - 1) / kWarpsPerBlock;
+unsigned grid_for(uint32_t nstreams, int nw, int per_sm, int num_sms) {
+    uint64_t want = (nstreams + nw - 1) / nw;
     uint64_t cap = (uint64_t)per_sm * num_sms;
     return (unsigned)std::max<uint64_t>(1, std::min(want, cap));
 }
 
-// Launch one bulk kernel over streams [b, e) of the handle.
+// Launch one bulk kernel over streams [b, e) of the handle.  Stream counts that fill every
+// SM with kBigBlock-warp blocks use those (one block per SM); smaller ones use 4-warp
+// blocks spread over all SMs.
 enum class Kind { BM1, BM2, BM3, POLAR, UNIFORM };
+
+template <int V>
+void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
+    if (ns >= (uint32_t)(kBigBlock * h->num_sms))
+        bm_kernel<V, kBigBlock><<<h->num_sms, kBigBlock * 32, bm_smem(kBigBlock), st>>>(p);
+    else
+        bm_kernel<V, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.bm[V], h->num_sms), kWarpsPerBlock * 32,
+                                       bm_smem(kWarpsPerBlock), st>>>(p);
+}
 
 cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st) {
     uint32_t ns = p.s_end - p.s_begin;
     switch (kind) {
-        case Kind::BM1:
-            bm_kernel<1><<<grid_for(ns, h->occ.bm1, h->num_sms), kWarpsPerBlock * 32, kBmSmem, st>>>(p);
-            break;
-        case Kind::BM2:
-            bm_kernel<2><<<grid_for(ns, h->occ.bm2, h->num_sms), kWarpsPerBlock * 32, kBmSmem, st>>>(p);
-            break;
-        case Kind::BM3:
-            bm_kernel<3><<<grid_for(ns, h->occ.bm3, h->num_sms), kWarpsPerBlock * 32, kBmSmem, st>>>(p);
-            break;
+        case Kind::BM1: launch_bm<1>(h, p, ns, st); break;
+        case Kind::BM2: launch_bm<2>(h, p, ns, st); break;
+        case Kind::BM3: launch_bm<3>(h, p, ns, st); break;
         case Kind::POLAR:
-            polar_kernel<<<grid_for(ns, h->occ.polar, h->num_sms), kWarpsPerBlock * 32, kPolarSmem, st>>>(p);
+            if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
+                polar_kernel<kBigBlockPolar>
+                    <<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
+            else
+                polar_kernel<kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.polar, h->num_sms),
+                                               kWarpsPerBlock * 32, polar_smem(kWarpsPerBlock), st>>>(p);
             break;
         case Kind::UNIFORM:
-            uniform_kernel<<<grid_for(ns, h->occ.uni, h->num_sms), kWarpsPerBlock * 32, kBmSmem, st>>>(p);
+            uniform_kernel<<<grid_for(ns, kWarpsPerBlock, h->occ.uni, h->num_sms), kWarpsPerBlock * 32, kUniSmem,
+                             st>>>(p);
             break;
     }
     h->launches += 1;
@@ -211,13 +223,17 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     h->S = S;
     h->variant = variant == 0 ? 1 : variant;
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
-    h->occ.bm1 = occupancy(bm_kernel<1>, kBmSmem);
-    h->occ.bm2 = occupancy(bm_kernel<2>, kBmSmem);
-    h->occ.bm3 = occupancy(bm_kernel<3>, kBmSmem);
-    h->occ.polar = occupancy(polar_kernel, kPolarSmem);
-    h->occ.uni = occupancy(uniform_kernel, kBmSmem);
-    h->occ.mask = occupancy(polar_mask_kernel, kBmSmem);
-    h->occ.init = occupancy(init_kernel, kInitSmem);
+    h->occ.bm[1] = occupancy(bm_kernel<1, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    h->occ.bm[2] = occupancy(bm_kernel<2, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    h->occ.bm[3] = occupancy(bm_kernel<3, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    h->occ.polar = occupancy(polar_kernel<kWarpsPerBlock>, kWarpsPerBlock, polar_smem(kWarpsPerBlock));
+    occupancy(bm_kernel<1, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
+    occupancy(bm_kernel<2, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
+    occupancy(bm_kernel<3, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
+    occupancy(polar_kernel<kBigBlockPolar>, kBigBlockPolar, polar_smem(kBigBlockPolar));
+    h->occ.uni = occupancy(uniform_kernel, kWarpsPerBlock, kUniSmem);
+    h->occ.mask = occupancy(polar_mask_kernel, kWarpsPerBlock, kUniSmem);
+    h->occ.init = occupancy(init_kernel, kWarpsPerBlock, kInitSmem);
     if (cudaMalloc(&h->ring, (size_t)S * kPitch * sizeof(uint64_t)) != cudaSuccess ||
         cudaMalloc(&h->count, (size_t)S * sizeof(uint64_t)) != cudaSuccess) {
         cudaGetLastError();
@@ -226,7 +242,7 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
         set_err(NRNG_ENOMEM);
         return nullptr;
     }
-    init_kernel<<<grid_for(S, h->occ.init, h->num_sms), kWarpsPerBlock * 32, kInitSmem, h->stream>>>(
+    init_kernel<<<grid_for(S, kWarpsPerBlock, h->occ.init, h->num_sms), kWarpsPerBlock * 32, kInitSmem, h->stream>>>(
         h->ring, h->count, seed, first, S);
     h->launches += 1;
     cudaError_t e = cudaGetLastError();
@@ -310,7 +326,8 @@ int nrng_polar_mask(nrng_handle h, uint8_t* dev_mask, size_t cand_per_stream) {
     p.count = h->count;
     p.s_begin = 0;
     p.s_end = h->S;
-    polar_mask_kernel<<<grid_for(h->S, h->occ.mask, h->num_sms), kWarpsPerBlock * 32, kBmSmem, h->stream>>>(
+    polar_mask_kernel<<<grid_for(h->S, kWarpsPerBlock, h->occ.mask, h->num_sms), kWarpsPerBlock * 32, kUniSmem,
+                        h->stream>>>(
         p, dev_mask, cand_per_stream);
     h->launches += 1;
     return cuda_err(cudaGetLastError());

@@ -22,9 +22,13 @@ struct BulkParams {
     int aligned;
 };
 
-// Per-block shared memory: [kWarpsPerBlock x kWin u64 windows][ln table][per-kernel extras].
-constexpr size_t kWinBytes = kWarpsPerBlock * kWinAlloc * sizeof(uint64_t);
-constexpr size_t kTabBytes = kLogTableEntries * sizeof(double2);
+// Per-block shared memory: [NW x kWinAlloc u64 windows][tables][per-kernel extras].
+// The bulk kernels come in two block shapes: NW = 4 warps (small stream counts: spread
+// over all SMs) and NW = kBigBlock warps, one block per SM (the tables are stored once per
+// SM instead of once per 4 warps, which is what lets 20 windows fit in 227 KB).
+constexpr size_t win_bytes(int nw) { return (size_t)nw * kWinAlloc * sizeof(uint64_t); }
+constexpr int kBigBlock = 20;
+constexpr int kBigBlockPolar = 16;
 
 // ------------------------------------------------------------------ seeding + warm-up
 // Word j of global stream g = splitmix64 output #(607 g + j) of seed (R2); all-even fix
@@ -71,7 +75,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) init_kernel(uint64_t* __r
 // and the stream holding the dropped last deviate of an odd n take the 32-pair path.
 // U pairs per lane: pair u reads its words at src + u * 32 * per (lane-interleaved).
 template <int V, int U>
-__device__ __forceinline__ void bm_pairs(const uint64_t* src, const TParams& tp, const double2* tab, double (&x)[U],
+__device__ __forceinline__ void bm_pairs(const uint64_t* src, const TParams& tp, const Tables& tab, double (&x)[U],
                                          double (&y)[U]) {
     constexpr int per = (V == 3) ? 3 : 2;
     if (V == 3) {
@@ -98,8 +102,8 @@ __device__ __forceinline__ void bm_pairs(const uint64_t* src, const TParams& tp,
     }
 }
 
-template <int V>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 5) bm_kernel(BulkParams p) {
+template <int V, int NW>
+__global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr uint32_t per = (V == 3) ? 3 : 2;
@@ -108,13 +112,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 5) bm_kernel(BulkParams p
     constexpr uint32_t kNeedU = 32 * kU * per;         // words per main-loop iteration
     static_assert(kNeedU - 1 + kB <= kWin - kLagR, "lookahead would clobber the write-back words");
     static_assert(kNeedU <= kMirror, "unmasked reads must stay inside the mirror");
-    double2* tab = reinterpret_cast<double2*>(smem + kWarpsPerBlock * kWinAlloc);
-    load_log_table(tab);
+    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
     __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
-    for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
-         k += gridDim.x * kWarpsPerBlock) {
+    for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 5) bm_kernel(BulkParams p
 // them densely (two per lane; no lane idles on a rejected candidate) and stores 64
 // consecutive pairs.  The stream's last < 64 survivors are flushed 32 at a time.
 constexpr int kQueue = 128;
-constexpr size_t kQueueBytes = kWarpsPerBlock * 3 * kQueue * sizeof(double);
+constexpr size_t queue_bytes(int nw) { return (size_t)nw * 3 * kQueue * sizeof(double); }
 
 struct PolarQueue {
     double *x, *y, *s;
@@ -196,18 +198,17 @@ __device__ __forceinline__ uint32_t polar_append(bool ok, const PolarCand& c, in
     return used;
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 4) polar_kernel(BulkParams p) {
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double2* tab = reinterpret_cast<double2*>(smem + kWarpsPerBlock * kWinAlloc);
-    load_log_table(tab);
+    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
     __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
-    double* qb = reinterpret_cast<double*>(smem + kWarpsPerBlock * kWinAlloc + 2 * kLogTableEntries) + warp * 3 * kQueue;
+    double* qb = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + warp * 3 * kQueue;
     PolarQueue q{qb, qb + kQueue, qb + 2 * kQueue};
-    for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
-         k += gridDim.x * kWarpsPerBlock) {
+    for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
@@ -329,8 +330,8 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_mask_kernel(BulkPar
 __device__ __forceinline__ uint64_t word_of(double u) { return __double2ull_rn(u * 0x1p53) << 11; }
 __global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs, double* __restrict__ out,
                                  uint8_t* __restrict__ mask, TParams tp, int method) {
-    __shared__ double2 tab[kLogTableEntries];
-    load_log_table(tab);
+    __shared__ double2 tabs[kTabBytes / 16];
+    const Tables tab = load_tables(tabs);
     __syncthreads();
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_pairs;
          j += (uint64_t)gridDim.x * blockDim.x) {

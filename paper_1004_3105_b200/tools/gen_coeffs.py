@@ -87,7 +87,7 @@ def generate():
 # error (< 1e-16 absolute on the reduced arguments) sits far inside the 1e-13 output bar.
 
 LOG_BASE_HI = 0x3FE6A09E  # high word of sqrt(1/2): m is normalised into [sqrt(1/2), sqrt(2))
-LOG_TABLE_BITS = 7
+LOG_TABLE_BITS = 8
 
 
 def _d_from_hi(hi):
@@ -111,7 +111,7 @@ def log_table():
     return rows, float(rmax)
 
 
-def log1p_coeffs(rmax, degree=6):
+def log1p_coeffs(rmax, degree=5):
     """Taylor coefficients of ln(1+r) = r + sum_{k=2..degree} (-1)^(k+1) r^k / k; truncation
     error rmax^(degree+1)/(degree+1)."""
     err = rmax ** (degree + 1) / (degree + 1)
