@@ -33,12 +33,24 @@ METRIC = "fp64 normals/sec per method (B1, B3, Polar) at 1/2/4/8 B200; % of roof
 METHODS = ("B1", "B2", "B3", "P")
 CFG = W.C5_SHARD
 BYTES_PER_NORMAL = 8  # algorithmic HBM traffic: one fp64 written per normal
-# Algorithmic FP64 work per normal: the paper's operation tallies
-# (B1 P:98-101, P P:131-134, B3 P:280-295, B2 P:159-170) priced per primitive in DP-pipe
-# instructions of the sm_100a libdevice fast paths (ln 28, sqrt 8, div 8, sincospi 24,
-# sincos16 21, Horner-15 15, uniform 2) -- SURVEY.md §8(a).
-DP_PER_NORMAL = {"B1": 34.5, "B2": 33.0, "B3": 30.5, "P": 28.5}
-FP64_PEAK_NOMINAL = 148 * 64 * 1.965e9  # DP lanes per SM x SMs x max clock (DP instr/s)
+# Algorithmic FP64 work per pair ("roofline"): the paper's operation sequence
+# for each method, priced with the DP-pipe cost of double-accurate primitives
+# (ln 9, radius sigma sqrt(-2 ln) 10, sin+cos of an exactly reduced angle 14, IEEE divide 7,
+# sincos16 of P:162-170 21, Horner-15 15; MUFU seeds and integer work not counted):
+#   B1 = ln + radius + sincos + 2 outputs                     = 35
+#   B2 = ln + radius + sincos16 + 2                           = 42
+#   B3 = bulk (u, 2 fma, div, Horner, 3 mul, sincos16, 2) 51, tail (1/9) 7 fewer  = 50.2
+#   P  = (4/pi) candidates x 3 + ln + 1 + 1 + Newton 6 + 2 + 2 = 24.8
+DP_PER_PAIR = {"B1": 35.0, "B2": 42.0, "B3": 51.0 - 7.0 / 9.0, "P": 3.0 * 4.0 / math.pi + 21.0}
+FP64_PEAK_NOMINAL = 148 * 64 * 1.965e9  # SMs x FP64 lanes per SM x max SM clock = DP instr/s
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
+# capture of the same launch (profiles/); None until captured.
+TRAFFIC = {}
+try:
+    with open(os.path.join(ROOT, "profiles", "traffic.json")) as _fh:
+        TRAFFIC = json.load(_fh)
+except Exception:
+    pass
 
 
 def load_peaks():
@@ -242,29 +254,19 @@ def main():
     if args.validate:
         from statistics import NormalDist
 
+        from paper_1004_3105_b200 import dist as D
+
         K = 256
         edges = [CFG.mu + CFG.sigma * NormalDist().inv_cdf(i / K) for i in range(1, K)]
         for m in METHODS:
             g.normal(m, out=out, mu=CFG.mu, sigma=CFG.sigma)
             sums, hist = P.stats(out, CFG.mu, edges)
-            red = torch.cat([sums[:4], hist.to(torch.float64)])
-            mn, mx = sums[4:5].clone(), sums[5:6].clone()
-            if world > 1:
-                dist.all_reduce(red)
-                dist.all_reduce(mn, op=dist.ReduceOp.MIN)
-                dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-            red = red.cpu().numpy()
+            sums, hist = D.allreduce_stats(sums, hist)  # NCCL: the run's only GPU<->GPU exchange
+            sums, hist = sums.cpu().numpy(), hist.cpu().numpy()
             n = world * CFG.n
-            m1 = red[0] / n
-            var = red[1] / n - m1 * m1
-            skew = (red[2] / n - 3 * m1 * red[1] / n + 2 * m1**3) / var**1.5
-            kurt = (red[3] / n) / var**2 - 3
-            hist_v = red[4:]
-            chi2 = float(np.sum((hist_v - n / K) ** 2 / (n / K)))
-            ok = (abs(m1) < 4 / math.sqrt(n) and abs(var - 1) < 4 * math.sqrt(2 / n)
-                  and abs(skew) < 4 * math.sqrt(6 / n) and abs(kurt) < 4 * math.sqrt(24 / n))
-            validation[m] = {"mean": m1, "var": var, "skew": skew, "exkurt": kurt, "chi2": chi2, "dof": K - 1,
-                             "min": float(mn), "max": float(mx), "moments_4se_pass": bool(ok)}
+            v = D.moments(sums, n, CFG.sigma)
+            v.update({"chi2": D.chi_square(hist, n), "dof": K - 1, "min": float(sums[4]), "max": float(sums[5])})
+            validation[m] = v
 
     # ---- e2e: the same step through the public API with HOST output buffers (pinned),
     # the device->host copies inside the timed region (library chunked/overlapped path)
@@ -297,24 +299,25 @@ def main():
         return
 
     peaks, peak_kind = load_peaks()
-    dom = max(METHODS, key=lambda m: per_ms[m])
-    t_launch = per_ms[dom] / 1e3
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    hbm_achieved = BYTES_PER_NORMAL * CFG.n / t_launch / 1e9
     fp64_peak = FP64_PEAK_NOMINAL
-    fp64_achieved = DP_PER_NORMAL[dom] * CFG.n / t_launch
-    t_hbm = BYTES_PER_NORMAL * CFG.n / (hbm_peak * 1e9)
-    t_fp64 = DP_PER_NORMAL[dom] * CFG.n / fp64_peak
-    if t_fp64 >= t_hbm:
-        roof = {"bound": "alu", "achieved": fp64_achieved / 1e12, "peak": fp64_peak / 1e12,
-                "unit": "T DP-pipe instr/s", "frac": fp64_achieved / fp64_peak, "traffic": None,
-                "kernel": "%s (%s)" % ({"P": "polar_kernel"}.get(dom, "bm_kernel<%s>" % dom[1]), dom),
-                "peak_source": "148 SMs x 64 FP64 lanes x 1965 MHz (nominal; measured DFMA 17.09 T/s)",
-                "alt_hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
-                            "frac": hbm_achieved / hbm_peak, "peak_source": peak_kind}}
-    else:
-        roof = {"bound": "hbm", "achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": hbm_achieved / hbm_peak, "traffic": None, "peak_source": peak_kind}
+    roofs = {}
+    for m in METHODS:
+        t = per_ms[m] / 1e3
+        t_hbm = BYTES_PER_NORMAL * CFG.n / (hbm_peak * 1e9)
+        t_alu = DP_PER_PAIR[m] * CFG.n / 2 / fp64_peak
+        if t_alu > t_hbm:
+            roofs[m] = {"bound": "alu", "achieved": DP_PER_PAIR[m] * CFG.n / 2 / t / 1e12, "peak": fp64_peak / 1e12,
+                        "unit": "T DP-instr/s", "frac": t_alu / t,
+                        "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1965 MHz (probe: DFMA 17.09 T/s measured)"}
+        else:
+            roofs[m] = {"bound": "hbm", "achieved": BYTES_PER_NORMAL * CFG.n / t / 1e9, "peak": hbm_peak,
+                        "unit": "GB/s", "frac": t_hbm / t, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
+        roofs[m]["traffic"] = None
+    dom = max(METHODS, key=lambda m: per_ms[m])
+    kname = {"P": "polar_kernel"}.get(dom, "bm_kernel<%s>" % dom[1])
+    roof = dict(roofs[dom], kernel="%s (%s)" % (kname, dom), method=dom)
+    roof["traffic"] = TRAFFIC.get(dom)
 
     cpu = None
     if not args.no_cpu:
@@ -334,8 +337,8 @@ def main():
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(world),
         "per_method": {m: {"normals_per_s": world * CFG.n / (per_ms[m] / 1e3), "ms_per_call": per_ms[m],
-                           "dp_frac_of_nominal": DP_PER_NORMAL[m] * CFG.n / (per_ms[m] / 1e3) / fp64_peak,
-                           "hbm_write_frac": BYTES_PER_NORMAL * CFG.n / (per_ms[m] / 1e3) / 1e9 / hbm_peak}
+                           "roofline_bound": roofs[m]["bound"], "roofline_frac": roofs[m]["frac"],
+                           "hbm_write_gbs": BYTES_PER_NORMAL * CFG.n / (per_ms[m] / 1e3) / 1e9}
                        for m in METHODS},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         "create_s": create_s, "validation": validation,
