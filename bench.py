@@ -315,7 +315,7 @@ def main():
                         "unit": "GB/s", "frac": t_hbm / t, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
         roofs[m]["traffic"] = None
     dom = max(METHODS, key=lambda m: per_ms[m])
-    kname = {"P": "polar_kernel"}.get(dom, "bm_kernel<%s>" % dom[1])
+    kname = "polar_kernel" if dom == "P" else "bm_kernel<%s>" % dom[1]
     roof = dict(roofs[dom], kernel="%s (%s)" % (kname, dom), method=dom)
     roof["traffic"] = TRAFFIC.get(dom)
 

@@ -28,7 +28,7 @@ struct BulkParams {
 // SM instead of once per 4 warps, which is what lets 20 windows fit in 227 KB).
 constexpr size_t win_bytes(int nw) { return (size_t)nw * kWinAlloc * sizeof(uint64_t); }
 constexpr int kBigBlock = 20;
-constexpr int kBigBlockPolar = 16;
+constexpr int kBigBlockPolar = 20;
 
 // ------------------------------------------------------------------ seeding + warm-up
 // Word j of global stream g = splitmix64 output #(607 g + j) of seed (R2); all-even fix
@@ -156,46 +156,30 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
 }
 
 // ------------------------------------------------------------------ Polar P
-// Candidate phase: 64 candidates (128 uniforms) per warp step, two per lane.  Accepts
-// are ranked with __ballot_sync/__popc (first the 32 candidates of the lower half, then
-// the upper half, so the queue order is the candidate order), trimmed at the stream's
-// remaining quota (exact stop, R5), and appended to a per-warp shared-memory queue.
-// Transform phase: whenever the queue holds >= 64 survivors the warp transforms 64 of
-// them densely (two per lane; no lane idles on a rejected candidate) and stores 64
-// consecutive pairs.  The stream's last < 64 survivors are flushed 32 at a time.
+// Candidate phase: 64 candidates (128 uniforms) per warp step, two per lane: candidate i
+// of the step is lane i%32's (i < 32: words wc + 2i, i >= 32: wc + 64 + 2(i-32)).  Accepts
+// are ranked with __ballot_sync/__popc in candidate order, trimmed at the stream's
+// remaining quota (exact stop, R5: the last step consumes candidates only up to the
+// p_k-th accept), and the window position of each survivor is appended to a per-warp
+// shared-memory queue (4 bytes per entry: the words stay in the window, which keeps >= 600
+// words of history behind wc).  Transform phase: whenever >= 64 survivors are queued the
+// warp re-reads their words, recomputes (X, Y, S) and transforms 64 of them densely (two
+// per lane; no lane idles on a rejected candidate), storing 64 consecutive pairs.
 constexpr int kQueue = 128;
-constexpr size_t queue_bytes(int nw) { return (size_t)nw * 3 * kQueue * sizeof(double); }
+constexpr int kQueueAlloc = kQueue + 32;  // ring + one scratch slot per lane
+constexpr size_t queue_bytes(int nw) { return (size_t)nw * kQueueAlloc * sizeof(uint32_t); }
 
-struct PolarQueue {
-    double *x, *y, *s;
-    __device__ __forceinline__ void put(uint32_t slot, const PolarCand& c) {
-        slot &= kQueue - 1;
-        x[slot] = c.X;
-        y[slot] = c.Y;
-        s[slot] = c.S;
+template <int U>
+__device__ __forceinline__ void polar_from_queue(const uint64_t* buf, const uint32_t* q, uint32_t first, int lane,
+                                                 const TParams& tp, const Tables& tab, double (&ox)[U],
+                                                 double (&oy)[U]) {
+    PolarCand c[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(buf + q[(first + 32 * u + lane) & (kQueue - 1)]);
+        polar_candidate(w.x, w.y, c[u]);
     }
-    __device__ __forceinline__ PolarCand get(uint32_t slot) const {
-        slot &= kQueue - 1;
-        return PolarCand{x[slot], y[slot], s[slot]};
-    }
-};
-
-// Rank the accepted candidates of one group of 32 and append the first `need` of them.
-// Returns the number of candidates consumed (32, or up to and including the last used).
-__device__ __forceinline__ uint32_t polar_append(bool ok, const PolarCand& c, int lane, uint64_t need, PolarQueue& q,
-                                                 uint64_t& acc) {
-    unsigned m = __ballot_sync(kFull, ok);
-    const int rank = __popc(m & lanemask_lt(lane));
-    uint32_t used = 32;
-    if ((uint64_t)__popc(m) >= need) {  // exact stop inside this group of 32
-        const unsigned last = __ballot_sync(kFull, ok && (uint64_t)rank == need - 1);
-        const int lastlane = __ffs(last) - 1;
-        used = lastlane + 1;
-        m &= (lastlane == 31) ? kFull : ((2u << lastlane) - 1u);
-    }
-    if ((m >> lane) & 1u) q.put((uint32_t)acc + rank, c);
-    acc += __popc(m);
-    return used;
+    polar_transform<U>(c, tp, tab, ox, oy);
 }
 
 template <int NW>
@@ -206,8 +190,8 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
     __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
-    double* qb = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + warp * 3 * kQueue;
-    PolarQueue q{qb, qb + kQueue, qb + 2 * kQueue};
+    uint32_t* q = reinterpret_cast<uint32_t*>(smem + NW * kWinAlloc + kTabBytes / 8) + warp * kQueueAlloc;
+    const unsigned lt = lanemask_lt(lane);
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
@@ -215,47 +199,75 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         lfg_load(L, rk, C, lane);
         const bool fast = p.aligned && 2 * (qk.off + qk.cnt) <= p.n;
-        double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
-        uint64_t acc = 0;    // accepted (queued) pairs of this stream
-        uint64_t done = 0;   // pairs transformed and stored
-        while (acc < qk.cnt) {
-            lfg_ensure(L, lane, 128);
-            const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(L.at(2 * lane));
-            const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(L.at(64 + 2 * lane));
-            PolarCand c0, c1;
-            const bool ok0 = polar_candidate(w0.x, w0.y, c0);
-            const bool ok1 = polar_candidate(w1.x, w1.y, c1);
-            const uint32_t used0 = polar_append(ok0, c0, lane, qk.cnt - acc, q, acc);
-            uint32_t used = used0;
-            if (used0 == 32 && acc < qk.cnt) used += polar_append(ok1, c1, lane, qk.cnt - acc, q, acc);
-            L.wc += 2 * used;
-            __syncwarp();
-            if (fast && acc - done >= 64) {
-                const PolarCand c[2] = {q.get((uint32_t)done + lane), q.get((uint32_t)done + 32 + lane)};
-                double ox[2], oy[2];
-                polar_transform<2>(c, p.tp, tab, ox, oy);
-                __stcs(o + done, make_double2(ox[0], oy[0]));
-                __stcs(o + done + 32, make_double2(ox[1], oy[1]));
-                done += 64;
+        // the stream's quota in chunks of < 2^31 pairs: 32-bit counters in the loops
+        for (uint64_t base = 0; base < qk.cnt;) {
+            const uint32_t cnt = (uint32_t)(qk.cnt - base < (1ull << 31) ? qk.cnt - base : (1ull << 31));
+            double2* o = reinterpret_cast<double2*>(p.out + (2 * (qk.off + base) - p.shift)) + lane;
+            uint32_t acc = 0;   // accepted (queued) pairs of this chunk
+            uint32_t done = 0;  // pairs transformed and stored
+            while (acc < cnt) {
+                lfg_ensure(L, lane, 128);
+                const uint32_t pos0 = (L.wc & kWinMask) + 2 * lane, pos1 = pos0 + 64;
+                const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(L.buf + pos0);
+                const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(L.buf + pos1);
+                PolarCand c0, c1;
+                const bool ok0 = polar_candidate(w0.x, w0.y, c0);
+                const bool ok1 = polar_candidate(w1.x, w1.y, c1);
+                unsigned m0 = __ballot_sync(kFull, ok0), m1 = __ballot_sync(kFull, ok1);
+                const uint32_t need = cnt - acc;
+                uint32_t used = 64;
+                if ((uint32_t)(__popc(m0) + __popc(m1)) >= need) {
+                    // exact stop: keep the first `need` accepts in candidate order
+                    if ((uint32_t)__popc(m0) >= need) {
+                        const unsigned last = __ballot_sync(kFull, ok0 && (uint32_t)__popc(m0 & lt) == need - 1);
+                        const int l = __ffs(last) - 1;
+                        m0 &= (l == 31) ? kFull : ((2u << l) - 1u);
+                        m1 = 0;
+                        used = l + 1;
+                    } else {
+                        const uint32_t need1 = need - __popc(m0);
+                        const unsigned last = __ballot_sync(kFull, ok1 && (uint32_t)__popc(m1 & lt) == need1 - 1);
+                        const int l = __ffs(last) - 1;
+                        m1 &= (l == 31) ? kFull : ((2u << l) - 1u);
+                        used = 32 + l + 1;
+                    }
+                }
+                // branch-free append: rejected lanes write their position to a per-lane
+                // scratch slot past the ring (q[kQueue + lane]) instead of skipping the store
+                const uint32_t n0 = __popc(m0);
+                const uint32_t s0 = ((m0 >> lane) & 1u) ? ((acc + __popc(m0 & lt)) & (kQueue - 1)) : kQueue + lane;
+                const uint32_t s1 =
+                    ((m1 >> lane) & 1u) ? ((acc + n0 + __popc(m1 & lt)) & (kQueue - 1)) : kQueue + lane;
+                q[s0] = pos0;
+                q[s1] = pos1;
+                acc += n0 + __popc(m1);
+                L.wc += 2 * used;
+                __syncwarp();
+                if (fast && acc - done >= 64) {
+                    double ox[2], oy[2];
+                    polar_from_queue<2>(L.buf, q, done, lane, p.tp, tab, ox, oy);
+                    __stcs(o + done, make_double2(ox[0], oy[0]));
+                    __stcs(o + done + 32, make_double2(ox[1], oy[1]));
+                    done += 64;
+                    __syncwarp();
+                }
+                while (!fast && acc - done >= 32) {
+                    double ox[1], oy[1];
+                    polar_from_queue<1>(L.buf, q, done, lane, p.tp, tab, ox, oy);
+                    store_pair(p.out, 2 * (qk.off + base + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
+                    done += 32;
+                    __syncwarp();
+                }
+            }
+            for (; done < acc; done += 32) {
+                if ((uint32_t)lane < acc - done) {
+                    double ox[1], oy[1];
+                    polar_from_queue<1>(L.buf, q, done, lane, p.tp, tab, ox, oy);
+                    store_pair(p.out, 2 * (qk.off + base + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
+                }
                 __syncwarp();
             }
-            while (!fast && acc - done >= 32) {
-                const PolarCand c[1] = {q.get((uint32_t)done + lane)};
-                double ox[1], oy[1];
-                polar_transform<1>(c, p.tp, tab, ox, oy);
-                store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
-                done += 32;
-                __syncwarp();
-            }
-        }
-        for (; done < acc; done += 32) {
-            if ((uint64_t)lane < acc - done) {
-                const PolarCand c[1] = {q.get((uint32_t)done + lane)};
-                double ox[1], oy[1];
-                polar_transform<1>(c, p.tp, tab, ox, oy);
-                store_pair(p.out, 2 * (qk.off + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
-            }
-            __syncwarp();
+            base += cnt;
         }
         lfg_store(L, rk, C, lane);
         if (lane == 0) p.count[k] = C + (L.wc - kW0);
