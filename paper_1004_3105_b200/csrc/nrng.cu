@@ -100,6 +100,17 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
 
 cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st) {
     uint32_t ns = p.s_end - p.s_begin;
+    if (kind != Kind::UNIFORM && p.q + (p.rem ? 1 : 0) <= kTinyMaxPairs) {
+        const unsigned grid = (ns + kTinyThreads - 1) / kTinyThreads;
+        switch (kind) {
+            case Kind::BM1: tiny_kernel<1><<<grid, kTinyThreads, 0, st>>>(p); break;
+            case Kind::BM2: tiny_kernel<2><<<grid, kTinyThreads, 0, st>>>(p); break;
+            case Kind::BM3: tiny_kernel<3><<<grid, kTinyThreads, 0, st>>>(p); break;
+            default: tiny_kernel<4><<<grid, kTinyThreads, 0, st>>>(p); break;
+        }
+        h->launches += 1;
+        return cudaGetLastError();
+    }
     switch (kind) {
         case Kind::BM1: launch_bm<1>(h, p, ns, st); break;
         case Kind::BM2: launch_bm<2>(h, p, ns, st); break;

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
-        lfg_load(L, rk, C, lane);
+        lfg_load(L, rk, C, lane, qk.cnt * per < (uint64_t)kLagR ? (uint32_t)(qk.cnt * per) : (uint32_t)kLagR);
         uint64_t j0 = 0;
         if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
             double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
@@ -273,6 +273,72 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
         if (lane == 0) p.count[k] = C + (L.wc - kW0);
         __syncwarp();
     }
+}
+
+// ------------------------------------------------------------------ tiny quotas
+// Calls that give every stream only a few pairs (the C4 sweep: n <= 2^18 over 2^16
+// streams) are bound by per-stream latency and state traffic, not arithmetic: one THREAD
+// per stream generates its words straight through the HBM ring (x_{C+i} = ring[(C+i) mod
+// 607] + ring[(C+i+334) mod 607], written back in place -- exactly the recurrence, in the
+// canonical layout), transforms and stores.  Only the words actually used are touched.
+constexpr int kTinyThreads = 128;
+constexpr uint64_t kTinyMaxPairs = 4;  // per-stream quota routed here (8 words for B1)
+
+struct RingCursor {
+    uint64_t* r;
+    uint32_t a, b;  // positions of x_{n-607} (= slot of x_n) and x_{n-273}
+    __device__ __forceinline__ RingCursor(uint64_t* ring_k, uint64_t C) : r(ring_k) {
+        a = (uint32_t)(C % kLagR);
+        b = a + (kLagR - kLagS);
+        b = b >= (uint32_t)kLagR ? b - kLagR : b;
+    }
+    __device__ __forceinline__ uint64_t next() {
+        const uint64_t x = r[a] + r[b];
+        r[a] = x;
+        a = a + 1 == (uint32_t)kLagR ? 0 : a + 1;
+        b = b + 1 == (uint32_t)kLagR ? 0 : b + 1;
+        return x;
+    }
+};
+
+template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar
+__global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
+    __shared__ double2 tabs[kTabBytes / 16];
+    const Tables tab = load_tables(tabs);
+    __syncthreads();
+    const uint32_t k = p.s_begin + blockIdx.x * kTinyThreads + threadIdx.x;
+    if (k >= p.s_end) return;
+    const Quota qk = quota(p.q, p.rem, k);
+    if (qk.cnt == 0) return;
+    const uint64_t C = p.count[k];
+    RingCursor rc(p.ring + (uint64_t)k * kPitch, C);
+    uint64_t used = 0;
+    for (uint64_t j = 0; j < qk.cnt; ++j) {
+        double x[1], y[1];
+        if (V == 4) {
+            PolarCand c[1];
+            bool ok;
+            do {
+                const uint64_t wa = rc.next(), wb = rc.next();
+                used += 2;
+                ok = polar_candidate(wa, wb, c[0]);
+            } while (!ok);
+            polar_transform<1>(c, p.tp, tab, x, y);
+        } else if (V == 3) {
+            const uint64_t w1[1] = {rc.next()}, w2[1] = {rc.next()}, w3[1] = {rc.next()};
+            used += 3;
+            b3_pairs<1>(w1, w2, w3, p.tp, tab, x, y);
+        } else {
+            const uint64_t wu[1] = {rc.next()}, wv[1] = {rc.next()};
+            used += 2;
+            if (V == 1)
+                b1_pairs<1>(wu, wv, p.tp, tab, x, y);
+            else
+                b2_pairs<1>(wu, wv, p.tp, tab, x, y);
+        }
+        store_pair(p.out, 2 * (qk.off + j), p.shift, p.n, x[0], y[0], p.aligned);
+    }
+    p.count[k] = C + used;
 }
 
 // ------------------------------------------------------------------ test hooks

@@ -143,6 +143,18 @@ def test_c5_shard_bench_launch_sampled(method):
     del out
 
 
+def test_short_calls_partial_state_load():
+    # per-stream quotas of 5..100 pairs: warp kernel reading only the state words it needs
+    S = 512
+    for m in ("B1", "B2", "B3"):
+        g, st = P.Generator(31, S), O.Streams(31, S)
+        for pairs in (5, 17, 100, 3, 140):
+            d = gen_normals(g, m, 2 * S * pairs, 0.0, 1.0)
+            o = ora_normals(st, m, 2 * S * pairs, 0.0, 1.0)
+            assert np.max(np.abs(d - o)) <= tol_for(m)
+        assert_state_equal(g, st)
+
+
 def test_c4_sweep_sequence():
     c = W.C4
     g, st = P.Generator(c.seed, c.streams), O.Streams(c.seed, c.streams)
@@ -195,9 +207,10 @@ def test_zero_n_is_noop_and_sigma_zero():
         assert np.all(x == -4.5)
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 63, 64, 65, 127, 129, 2 * 64 * 33 + 1])
-@pytest.mark.parametrize("method", ["B1", "B3", "P"])
+@pytest.mark.parametrize("n", [1, 2, 3, 63, 64, 65, 127, 129, 2 * 64 * 4 + 1, 2 * 64 * 5 - 1, 2 * 64 * 33 + 1])
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P"])
 def test_small_and_odd_n(n, method):
+    # n <= 2 * 64 * 4: one thread per stream (tiny quotas); larger: warp per stream
     S = 64
     g, st = P.Generator(4, S), O.Streams(4, S)
     for _ in range(2):
