@@ -32,8 +32,8 @@ int cuda_err(cudaError_t e) {
     return set_err(NRNG_ECUDA);
 }
 
-constexpr size_t bm_smem(int nw) { return win_bytes(nw) + kTabBytes; }
-constexpr size_t polar_smem(int nw) { return bm_smem(nw) + queue_bytes(nw); }
+constexpr size_t bm_smem(int nw) { return win_bytes(nw) + kTabBytes + tailq_bytes(nw); }
+constexpr size_t polar_smem(int nw) { return win_bytes(nw) + kTabBytes + queue_bytes(nw); }
 constexpr size_t kUniSmem = win_bytes(kWarpsPerBlock);
 constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
 constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)

@@ -102,6 +102,35 @@ __device__ __forceinline__ void bm_pairs(const uint64_t* src, const TParams& tp,
     }
 }
 
+// B3 tail compaction (fast path only).  A pair with u > tau (prob. 1/9) needs ln + sqrt
+// instead of the Moebius/Horner bulk path; evaluating both for every lane would cost the
+// tail's ~33 instructions on every pair.  Instead the bulk pass leaves (c, s) in the tail
+// pair's output slot and appends the local index of its first word to a per-warp list;
+// every kTailEvery iterations (before those words can leave the window: the window keeps
+// >= 1024 - 319 words of history) the list is drained 32 entries per warp step: re-read
+// u1, u2 from the window, compute the radius, read back (c, s), write the final pair.
+constexpr int kTailEvery = 3;
+constexpr int kTailCap = kTailEvery * 64;  // entries per drain (U = 2: <= 64 per iteration)
+constexpr int kTailAlloc = kTailCap + 32;   // + one scratch slot per lane (branch-free append)
+constexpr size_t tailq_bytes(int nw) { return (size_t)nw * kTailAlloc * sizeof(uint32_t); }
+
+__device__ __forceinline__ void b3_tail_drain(const uint32_t* tq, uint32_t tn, const uint64_t* buf, double2* o0,
+                                              int lane, const TParams& tp, const Tables& tab) {
+    for (uint32_t base = 0; base < tn; base += 32) {
+        const bool act = base + lane < tn;
+        const uint32_t wl = act ? tq[base + lane] : kW0;
+        const uint64_t* src = buf + (wl & kWinMask);
+        const uint64_t k1 = ukey(src[0]), k2 = ukey(src[1]);
+        const uint64_t Mk[1] = {k1 > k2 ? k1 : k2};
+        const uint32_t j = (wl - kW0) / 3;
+        const double2 cs = act ? o0[j] : make_double2(0.0, 0.0);
+        const double c[1] = {cs.x}, s[1] = {cs.y};
+        double x[1], y[1];
+        b3_tail_finish<1>(Mk, c, s, tp, tab, x, y);
+        if (act) __stcs(o0 + j, make_double2(x[0], y[0]));
+    }
+}
+
 template <int V, int NW>
 __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
@@ -116,6 +145,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
     __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
+    uint32_t* tq = reinterpret_cast<uint32_t*>(smem + NW * kWinAlloc + kTabBytes / 8) + warp * kTailAlloc;
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
@@ -123,17 +153,53 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         lfg_load(L, rk, C, lane, qk.cnt * per < (uint64_t)kLagR ? (uint32_t)(qk.cnt * per) : (uint32_t)kLagR);
         uint64_t j0 = 0;
-        if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
-            double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
+        if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n && (V != 3 || qk.cnt * per < (1ull << 31))) {
+            double2* o0 = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift));
+            double2* o = o0 + lane;
             const uint64_t full = qk.cnt - qk.cnt % (32 * kU);
+            uint32_t tn = 0, it = 0;  // B3: queued tail pairs, iterations since the last drain
             for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
                 lfg_ensure<kB>(L, lane, kNeedU);
                 const uint64_t* src = L.at(per * lane);
                 double x[kU], y[kU];
-                bm_pairs<V, kU>(src, p.tp, tab, x, y);
+                if (V == 3) {
+                    uint64_t w1[kU], w2[kU], w3[kU], Mk[kU];
+                    bool tail[kU];
 #pragma unroll
-                for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+                    for (int u = 0; u < kU; ++u) {
+                        w1[u] = src[32 * per * u];
+                        w2[u] = src[32 * per * u + 1];
+                        w3[u] = src[32 * per * u + 2];
+                    }
+                    b3_bulk<kU>(w1, w2, w3, p.tp, x, y, tail, Mk);
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+                    // branch-free append of the tail pairs' first-word local indices
+                    const uint32_t wl = L.wc + per * lane;
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const unsigned m = __ballot_sync(kFull, tail[u]);
+                        const uint32_t slot = tail[u] ? tn + __popc(m & lanemask_lt(lane)) : kTailCap + lane;
+                        tq[slot] = wl + 32 * per * u;
+                        tn += __popc(m);
+                    }
+                    if (++it == kTailEvery) {
+                        __syncwarp();
+                        b3_tail_drain(tq, tn, L.buf, o0, lane, p.tp, tab);
+                        tn = 0;
+                        it = 0;
+                    }
+                } else {
+                    bm_pairs<V, kU>(src, p.tp, tab, x, y);
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+                }
                 L.wc += kNeedU;
+                __syncwarp();
+            }
+            if (V == 3 && tn > 0) {
+                __syncwarp();
+                b3_tail_drain(tq, tn, L.buf, o0, lane, p.tp, tab);
                 __syncwarp();
             }
         }
