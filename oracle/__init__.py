@@ -65,6 +65,8 @@ def lib():
             "orc_polar_pair": ([dbl, dbl, dbl, dbl, p, p], C.c_int),
             "orc_normal_boxmuller": ([p, u32, p, u64, dbl, dbl, C.c_int], C.c_int),
             "orc_normal_polar": ([p, u32, p, u64, dbl, dbl], C.c_int),
+            "orc_normal_polar2": ([p, u32, p, u64, dbl, dbl], C.c_int),
+            "orc_polar2_pair": ([dbl, dbl, dbl, dbl, p, p], C.c_int),
             "orc_polar_mask": ([p, u32, p, u64], None),
             "orc_transform_from_uniforms": ([p, u64, p, p, dbl, dbl, C.c_int], C.c_int),
             "orc_stats": ([p, u64, dbl, p, C.c_int, p, p], None),
@@ -142,6 +144,11 @@ class Streams:
         lib().orc_normal_polar(_ptr(self.st), self.S, _ptr(out), n, mu, sigma)
         return out
 
+    def normal_polar2(self, n: int, mu: float = 0.0, sigma: float = 1.0) -> np.ndarray:
+        out = np.empty(n, np.float64)
+        lib().orc_normal_polar2(_ptr(self.st), self.S, _ptr(out), n, mu, sigma)
+        return out
+
     def polar_mask(self, cand_per_stream: int) -> np.ndarray:
         m = np.empty(self.S * cand_per_stream, np.uint8)
         lib().orc_polar_mask(_ptr(self.st), self.S, _ptr(m), cand_per_stream)
@@ -187,13 +194,20 @@ def polar_pair(a, b, mu=0.0, sigma=1.0):
     return bool(acc), ((float(xy[0]), float(xy[1])) if acc else None), tuple(float(t) for t in xys)
 
 
+def polar2_pair(a, b, mu=0.0, sigma=1.0):
+    """Method P2 on one candidate: (accepted, (x_out, y_out) or None, (x, y, s))."""
+    xy, xys = np.empty(2), np.empty(3)
+    acc = lib().orc_polar2_pair(a, b, mu, sigma, _ptr(xy), _ptr(xys))
+    return bool(acc), ((float(xy[0]), float(xy[1])) if acc else None), tuple(float(t) for t in xys)
+
+
 def transform_from_uniforms(u: np.ndarray, method: int, mu=0.0, sigma=1.0):
-    """method 1/2/3 = B1/B2/B3, 4 = Polar.  Returns (out[2*pairs], mask or None)."""
+    """method 1/2/3 = B1/B2/B3, 4 = Polar, 5 = P2.  Returns (out[2*pairs], mask or None)."""
     u = np.ascontiguousarray(u, np.float64)
     per = 3 if method == 3 else 2
     npairs = u.size // per
     out = np.empty(2 * npairs)
-    mask = np.empty(npairs, np.uint8) if method == 4 else None
+    mask = np.empty(npairs, np.uint8) if method >= 4 else None
     rc = lib().orc_transform_from_uniforms(_ptr(u), npairs, _ptr(out), _ptr(mask) if mask is not None else None,
                                            mu, sigma, method)
     if rc != 0:

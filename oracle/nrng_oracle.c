@@ -26,6 +26,8 @@
  *                 mu + s r sqrt2.
  *   P   P:108-119 x,y in [-1,1), s = x^2+y^2, reject s >= 1,
  *                 r = sigma sqrt(-2 ln(s)/s), return r x + mu, r y + mu.
+ *   P2  P:367-385 as P, but s > 8/9 -> r = sigma sqrt(-ln(1-s)/s), else r = sigma h(v(s));
+ *                 return x r sqrt2 + mu, y r sqrt2 + mu.
  * Work partition (stream-major, exact-stop; R5/R18): P = ceil(n/2) pairs,
  * stream k yields p_k = q + [k < rem] pairs at out[off_k + 2j], off_k = 2(kq+min(k,rem)).
  */
@@ -251,11 +253,36 @@ static void polar_transform(double x, double y, double s, double mu, double sigm
     *oy = fma(r, y, mu);
 }
 
+/* Method P2, P:367-385 (step 4a: r = sigma sqrt(-2 ln(u)/s) with u = 1 - s):
+ * 4.1 s > 8/9: r = sigma sqrt(-ln(1-s)/s) (library ln/sqrt; 1-s exact by Sterbenz);
+ * 4.2 else: v = (6s-4)/(4-3s) (reading R15's rounding), r = sigma h(v);
+ * 5.  return x r sqrt2 + mu, y r sqrt2 + mu, A = RN(r sqrt2) (reading R22).
+ * s == 0 needs no special case: v = -1, h(-1) ~ 1 and x = y = 0 give (mu, mu). */
+static void p2_transform(double x, double y, double s, double mu, double sigma, double* ox, double* oy) {
+    double r;
+    if (s > ORC_TAU) {
+        double w = 1.0 - s;
+        double q = -log(w) / s;
+        r = sigma * sqrt(q);
+    } else {
+        double v = orc_mobius(s);
+        r = sigma * orc_eval_h(v);
+    }
+    double A = r * ORC_SQRT2;
+    *ox = fma(x, A, mu);
+    *oy = fma(y, A, mu);
+}
+
 /* Exported single-pair transforms for closed-form pins (no stream involved). */
 void orc_b1_pair(double u, double v, double mu, double sigma, double* xy) { b1_pair(u, v, mu, sigma, &xy[0], &xy[1]); }
 void orc_b2_pair(double u, double v, double mu, double sigma, double* xy) { b2_pair(u, v, mu, sigma, &xy[0], &xy[1]); }
 void orc_b3_pair(double u1, double u2, double u3, double mu, double sigma, double* xy) {
     b3_pair(u1, u2, u3, mu, sigma, &xy[0], &xy[1]);
+}
+int orc_polar2_pair(double a, double b, double mu, double sigma, double* xy, double* xys) {
+    int acc = polar_candidate(a, b, &xys[0], &xys[1], &xys[2]);
+    if (acc) p2_transform(xys[0], xys[1], xys[2], mu, sigma, &xy[0], &xy[1]);
+    return acc;
 }
 /* returns accept; xy = outputs when accepted; xys = (x, y, s) */
 int orc_polar_pair(double a, double b, double mu, double sigma, double* xy, double* xys) {
@@ -324,6 +351,28 @@ int orc_normal_polar(orc_stream* st, uint32_t S, double* out, uint64_t n, double
     return 0;
 }
 
+/* Method P2 with the same candidate stream, acceptance and exact stop as Algorithm P. */
+int orc_normal_polar2(orc_stream* st, uint32_t S, double* out, uint64_t n, double mu, double sigma) {
+    uint64_t P = (n + 1) / 2;
+#pragma omp parallel for schedule(static)
+    for (long k = 0; k < (long)S; ++k) {
+        uint64_t cnt, off;
+        quota(P, S, (uint32_t)k, &cnt, &off);
+        uint64_t j = 0;
+        while (j < cnt) {
+            double a = next_uniform(&st[k]);
+            double b = next_uniform(&st[k]);
+            double x, y, s;
+            if (!polar_candidate(a, b, &x, &y, &s)) continue;
+            double ox, oy;
+            p2_transform(x, y, s, mu, sigma, &ox, &oy);
+            put_pair(out, n, 2 * (off + j), ox, oy);
+            ++j;
+        }
+    }
+    return 0;
+}
+
 /* Accept mask of exactly `cand` candidates per stream (2 uniforms each), stream-major. */
 void orc_polar_mask(orc_stream* st, uint32_t S, uint8_t* mask, uint64_t cand) {
 #pragma omp parallel for schedule(static)
@@ -337,11 +386,11 @@ void orc_polar_mask(orc_stream* st, uint32_t S, uint8_t* mask, uint64_t cand) {
     }
 }
 
-/* Transforms on caller-given uniforms: B1/B2/P use 2 per pair, B3 3 per pair.
- * method: 1,2,3 = B1,B2,B3; 4 = P (rejected candidates give NaN, NaN and mask 0). */
+/* Transforms on caller-given uniforms: B1/B2/P/P2 use 2 per pair, B3 3 per pair.
+ * method: 1,2,3 = B1,B2,B3; 4 = P, 5 = P2 (rejected candidates give NaN, NaN and mask 0). */
 int orc_transform_from_uniforms(const double* u, uint64_t n_pairs, double* out, uint8_t* mask, double mu,
                                 double sigma, int method) {
-    if (method < 1 || method > 4) return -1;
+    if (method < 1 || method > 5) return -1;
 #pragma omp parallel for schedule(static)
     for (long j = 0; j < (long)n_pairs; ++j) {
         double x = NAN, y = NAN;
@@ -352,7 +401,10 @@ int orc_transform_from_uniforms(const double* u, uint64_t n_pairs, double* out, 
             double cx, cy, s;
             int acc = polar_candidate(u[2 * j], u[2 * j + 1], &cx, &cy, &s);
             if (mask) mask[j] = (uint8_t)acc;
-            if (acc) polar_transform(cx, cy, s, mu, sigma, &x, &y);
+            if (acc) {
+                if (method == 4) polar_transform(cx, cy, s, mu, sigma, &x, &y);
+                else p2_transform(cx, cy, s, mu, sigma, &x, &y);
+            }
         }
         out[2 * j] = x;
         out[2 * j + 1] = y;
