@@ -60,7 +60,7 @@ extern "C" {
 
 typedef struct nrng_gen* nrng_handle;
 
-enum { NRNG_DEFAULT = 0, NRNG_B1 = 1, NRNG_B2 = 2, NRNG_B3 = 3, NRNG_POLAR = 4 };
+enum { NRNG_DEFAULT = 0, NRNG_B1 = 1, NRNG_B2 = 2, NRNG_B3 = 3, NRNG_POLAR = 4, NRNG_POLAR2 = 5 };
 enum { NRNG_OK = 0, NRNG_EINVAL = -1, NRNG_ENOMEM = -2, NRNG_ECUDA = -3, NRNG_ENODEV = -4 };
 
 #define NRNG_LAG_R 607        /* long lag: words of state per stream */
@@ -92,6 +92,13 @@ int nrng_normal_boxmuller(nrng_handle h, double* out, size_t n, double mu, doubl
 /* n deviates by the Polar method P with rejection compaction and exact stop. */
 int nrng_normal_polar(nrng_handle h, double* out, size_t n, double mu, double sigma);
 
+/* n deviates by method P2: the same candidates, acceptance
+ * and exact stop as nrng_normal_polar (identical uniform consumption), with step 4a
+ * (u = 1 - s): s <= 8/9 -> r = sigma h((6s-4)/(4-3s)) (B3's polynomial, bit-exact
+ * with the definition), s > 8/9 -> r = sigma sqrt(-ln(1-s)/s); returns x r sqrt2 + mu,
+ * y r sqrt2 + mu.  Errors as nrng_normal_polar. */
+int nrng_normal_polar2(nrng_handle h, double* out, size_t n, double mu, double sigma);
+
 /* Thread-local status of the last nrng_* call on this thread, and its text. */
 int nrng_last_error(void);
 const char* nrng_error_string(int code);
@@ -118,8 +125,8 @@ int nrng_uniform(nrng_handle h, double* out, size_t n);
  * dev_mask[k*cand_per_stream + j] = 1 iff candidate j of stream k is accepted (s < 1). */
 int nrng_polar_mask(nrng_handle h, uint8_t* dev_mask, size_t cand_per_stream);
 /* Transforms on caller-given device uniforms (no generator state involved):
- * method 1/2/3 = B1/B2/B3 (2/2/3 uniforms per pair), 4 = Polar candidate (2 uniforms;
- * rejected -> NaN outputs and dev_mask 0; dev_mask may be NULL).  out: 2*n_pairs.
+ * method 1/2/3 = B1/B2/B3 (2/2/3 uniforms per pair), 4 = Polar candidate, 5 = P2 candidate
+ * (2 uniforms; rejected -> NaN outputs and dev_mask 0; dev_mask may be NULL).  out: 2*n_pairs.
  * Enqueued on cuda_stream. */
 int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* dev_out, uint8_t* dev_mask,
                                  double mu, double sigma, int method, void* cuda_stream);

@@ -18,10 +18,10 @@ import numpy as np
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libnrng.so")
 
-NRNG_DEFAULT, NRNG_B1, NRNG_B2, NRNG_B3, NRNG_POLAR = 0, 1, 2, 3, 4
+NRNG_DEFAULT, NRNG_B1, NRNG_B2, NRNG_B3, NRNG_POLAR, NRNG_POLAR2 = 0, 1, 2, 3, 4, 5
 NRNG_OK, NRNG_EINVAL, NRNG_ENOMEM, NRNG_ECUDA, NRNG_ENODEV = 0, -1, -2, -3, -4
 LAG_R = 607
-METHODS = {"B1": 1, "B2": 2, "B3": 3, "P": 4}
+METHODS = {"B1": 1, "B2": 2, "B3": 3, "P": 4, "P2": 5}
 
 # name -> (argtypes, restype); mirrors include/nrng.h one to one
 _u64, _u32, _dbl, _p, _int, _sz = C.c_uint64, C.c_uint32, C.c_double, C.c_void_p, C.c_int, C.c_size_t
@@ -32,6 +32,7 @@ SIGNATURES = {
     "nrng_set_stream": ([_p, _p], _int),
     "nrng_normal_boxmuller": ([_p, _p, _sz, _dbl, _dbl, _int], _int),
     "nrng_normal_polar": ([_p, _p, _sz, _dbl, _dbl], _int),
+    "nrng_normal_polar2": ([_p, _p, _sz, _dbl, _dbl], _int),
     "nrng_last_error": ([], _int),
     "nrng_error_string": ([_int], C.c_char_p),
     "nrng_num_streams": ([_p], _u32),
@@ -113,6 +114,10 @@ def nrng_normal_boxmuller(h, out_ptr: int, n: int, mu: float, sigma: float, vari
 
 def nrng_normal_polar(h, out_ptr: int, n: int, mu: float, sigma: float) -> None:
     _check(lib().nrng_normal_polar(h, out_ptr, n, mu, sigma), "nrng_normal_polar")
+
+
+def nrng_normal_polar2(h, out_ptr: int, n: int, mu: float, sigma: float) -> None:
+    _check(lib().nrng_normal_polar2(h, out_ptr, n, mu, sigma), "nrng_normal_polar2")
 
 
 def nrng_uniform(h, out_ptr: int, n: int) -> None:
@@ -237,9 +242,17 @@ class Generator:
         nrng_normal_polar(self.h, ptr, n, mu, sigma)
         return out
 
+    def normal_polar2(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
+        out, ptr, n = self._out(n, out)
+        self._sync_stream()
+        nrng_normal_polar2(self.h, ptr, n, mu, sigma)
+        return out
+
     def normal(self, method: str, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
         if method == "P":
             return self.normal_polar(n, mu, sigma, out=out)
+        if method == "P2":
+            return self.normal_polar2(n, mu, sigma, out=out)
         return self.normal_boxmuller(n, mu, sigma, METHODS[method], out=out)
 
     def uniform(self, n: int = None, out=None):
@@ -273,12 +286,12 @@ class Generator:
 
 
 def transform_from_uniforms(u, method: int, mu: float = 0.0, sigma: float = 1.0):
-    """Device transform on given uniforms: method 1/2/3 = B1/B2/B3, 4 = Polar.  Returns (out, mask)."""
+    """Device transform on given uniforms: method 1/2/3 = B1/B2/B3, 4 = Polar, 5 = P2.  Returns (out, mask)."""
     torch = _torch()
     per = 3 if method == 3 else 2
     n_pairs = u.numel() // per
     out = torch.empty(2 * n_pairs, dtype=torch.float64, device=u.device)
-    mask = torch.empty(n_pairs, dtype=torch.uint8, device=u.device) if method == 4 else None
+    mask = torch.empty(n_pairs, dtype=torch.uint8, device=u.device) if method >= 4 else None
     nrng_transform_from_uniforms(u.data_ptr(), n_pairs, out.data_ptr(), mask.data_ptr() if mask is not None else None,
                                  mu, sigma, method, _stream_ptr(torch))
     return out, mask

@@ -87,7 +87,7 @@ unsigned grid_for(uint32_t nstreams, int nw, int per_sm, int num_sms) {
 // Launch one bulk kernel over streams [b, e) of the handle.  Stream counts that fill every
 // SM with kBigBlock-warp blocks use those (one block per SM); smaller ones use 4-warp
 // blocks spread over all SMs.
-enum class Kind { BM1, BM2, BM3, POLAR, UNIFORM };
+enum class Kind { BM1, BM2, BM3, POLAR, POLAR2, UNIFORM };
 
 template <int V>
 void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
@@ -98,6 +98,15 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
                                        bm_smem(kWarpsPerBlock), st>>>(p);
 }
 
+template <int M>
+void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
+    if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
+        polar_kernel<kBigBlockPolar, M><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
+    else
+        polar_kernel<kWarpsPerBlock, M><<<grid_for(ns, kWarpsPerBlock, h->occ.polar, h->num_sms),
+                                          kWarpsPerBlock * 32, polar_smem(kWarpsPerBlock), st>>>(p);
+}
+
 cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st) {
     uint32_t ns = p.s_end - p.s_begin;
     if (kind != Kind::UNIFORM && p.q + (p.rem ? 1 : 0) <= kTinyMaxPairs) {
@@ -106,6 +115,7 @@ cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st)
             case Kind::BM1: tiny_kernel<1><<<grid, kTinyThreads, 0, st>>>(p); break;
             case Kind::BM2: tiny_kernel<2><<<grid, kTinyThreads, 0, st>>>(p); break;
             case Kind::BM3: tiny_kernel<3><<<grid, kTinyThreads, 0, st>>>(p); break;
+            case Kind::POLAR2: tiny_kernel<5><<<grid, kTinyThreads, 0, st>>>(p); break;
             default: tiny_kernel<4><<<grid, kTinyThreads, 0, st>>>(p); break;
         }
         h->launches += 1;
@@ -115,14 +125,8 @@ cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st)
         case Kind::BM1: launch_bm<1>(h, p, ns, st); break;
         case Kind::BM2: launch_bm<2>(h, p, ns, st); break;
         case Kind::BM3: launch_bm<3>(h, p, ns, st); break;
-        case Kind::POLAR:
-            if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
-                polar_kernel<kBigBlockPolar>
-                    <<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
-            else
-                polar_kernel<kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.polar, h->num_sms),
-                                               kWarpsPerBlock * 32, polar_smem(kWarpsPerBlock), st>>>(p);
-            break;
+        case Kind::POLAR: launch_polar<1>(h, p, ns, st); break;
+        case Kind::POLAR2: launch_polar<2>(h, p, ns, st); break;
         case Kind::UNIFORM:
             uniform_kernel<<<grid_for(ns, kWarpsPerBlock, h->occ.uni, h->num_sms), kWarpsPerBlock * 32, kUniSmem,
                              st>>>(p);
@@ -237,11 +241,13 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     h->occ.bm[1] = occupancy(bm_kernel<1, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     h->occ.bm[2] = occupancy(bm_kernel<2, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     h->occ.bm[3] = occupancy(bm_kernel<3, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
-    h->occ.polar = occupancy(polar_kernel<kWarpsPerBlock>, kWarpsPerBlock, polar_smem(kWarpsPerBlock));
+    h->occ.polar = occupancy(polar_kernel<kWarpsPerBlock, 1>, kWarpsPerBlock, polar_smem(kWarpsPerBlock));
+    occupancy(polar_kernel<kWarpsPerBlock, 2>, kWarpsPerBlock, polar_smem(kWarpsPerBlock));
     occupancy(bm_kernel<1, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(bm_kernel<2, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(bm_kernel<3, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
-    occupancy(polar_kernel<kBigBlockPolar>, kBigBlockPolar, polar_smem(kBigBlockPolar));
+    occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));
+    occupancy(polar_kernel<kBigBlockPolar, 2>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     h->occ.uni = occupancy(uniform_kernel, kWarpsPerBlock, kUniSmem);
     h->occ.mask = occupancy(polar_mask_kernel, kWarpsPerBlock, kUniSmem);
     h->occ.init = occupancy(init_kernel, kWarpsPerBlock, kInitSmem);
@@ -321,6 +327,13 @@ int nrng_normal_polar(nrng_handle h, double* out, size_t n, double mu, double si
     return run_bulk(h, Kind::POLAR, out, n, (n + 1) / 2, 2, mu, sigma);
 }
 
+int nrng_normal_polar2(nrng_handle h, double* out, size_t n, double mu, double sigma) {
+    if (!h || (n > 0 && !out) || bad_params(mu, sigma)) return set_err(NRNG_EINVAL);
+    if (!check_device(h)) return set_err(NRNG_EINVAL);
+    if (n == 0) return set_err(NRNG_OK);
+    return run_bulk(h, Kind::POLAR2, out, n, (n + 1) / 2, 2, mu, sigma);
+}
+
 int nrng_uniform(nrng_handle h, double* out, size_t n) {
     if (!h || (n > 0 && !out)) return set_err(NRNG_EINVAL);
     if (!check_device(h)) return set_err(NRNG_EINVAL);
@@ -346,7 +359,7 @@ int nrng_polar_mask(nrng_handle h, uint8_t* dev_mask, size_t cand_per_stream) {
 
 int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* dev_out, uint8_t* dev_mask, double mu,
                                  double sigma, int method, void* cuda_stream) {
-    if ((n_pairs > 0 && (!dev_u || !dev_out)) || bad_params(mu, sigma) || method < 1 || method > 4)
+    if ((n_pairs > 0 && (!dev_u || !dev_out)) || bad_params(mu, sigma) || method < 1 || method > 5)
         return set_err(NRNG_EINVAL);
     if (n_pairs == 0) return set_err(NRNG_OK);
     int dev = 0, sms = 148;

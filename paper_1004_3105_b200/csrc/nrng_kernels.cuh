@@ -235,7 +235,7 @@ constexpr int kQueue = 128;
 constexpr int kQueueAlloc = kQueue + 32;  // ring + one scratch slot per lane
 constexpr size_t queue_bytes(int nw) { return (size_t)nw * kQueueAlloc * sizeof(uint32_t); }
 
-template <int U>
+template <int U, int M>
 __device__ __forceinline__ void polar_from_queue(const uint64_t* buf, const uint32_t* q, uint32_t first, int lane,
                                                  const TParams& tp, const Tables& tab, double (&ox)[U],
                                                  double (&oy)[U]) {
@@ -245,10 +245,14 @@ __device__ __forceinline__ void polar_from_queue(const uint64_t* buf, const uint
         const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(buf + q[(first + 32 * u + lane) & (kQueue - 1)]);
         polar_candidate(w.x, w.y, c[u]);
     }
-    polar_transform<U>(c, tp, tab, ox, oy);
+    if (M == 2)
+        p2_transform<U>(c, tp, tab, ox, oy);
+    else
+        polar_transform<U>(c, tp, tab, ox, oy);
 }
 
-template <int NW>
+// M = 1: Algorithm P (= the paper's P1); M = 2: method P2, same candidates.
+template <int NW, int M>
 __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 __syncwarp();
                 if (fast && acc - done >= 64) {
                     double ox[2], oy[2];
-                    polar_from_queue<2>(L.buf, q, done, lane, p.tp, tab, ox, oy);
+                    polar_from_queue<2, M>(L.buf, q, done, lane, p.tp, tab, ox, oy);
                     __stcs(o + done, make_double2(ox[0], oy[0]));
                     __stcs(o + done + 32, make_double2(ox[1], oy[1]));
                     done += 64;
@@ -319,7 +323,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 }
                 while (!fast && acc - done >= 32) {
                     double ox[1], oy[1];
-                    polar_from_queue<1>(L.buf, q, done, lane, p.tp, tab, ox, oy);
+                    polar_from_queue<1, M>(L.buf, q, done, lane, p.tp, tab, ox, oy);
                     store_pair(p.out, 2 * (qk.off + base + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
                     done += 32;
                     __syncwarp();
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
             for (; done < acc; done += 32) {
                 if ((uint32_t)lane < acc - done) {
                     double ox[1], oy[1];
-                    polar_from_queue<1>(L.buf, q, done, lane, p.tp, tab, ox, oy);
+                    polar_from_queue<1, M>(L.buf, q, done, lane, p.tp, tab, ox, oy);
                     store_pair(p.out, 2 * (qk.off + base + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
                 }
                 __syncwarp();
@@ -367,7 +371,7 @@ struct RingCursor {
     }
 };
 
-template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar
+template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2
 __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
     __shared__ double2 tabs[kTabBytes / 16];
     const Tables tab = load_tables(tabs);
@@ -381,7 +385,7 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
     uint64_t used = 0;
     for (uint64_t j = 0; j < qk.cnt; ++j) {
         double x[1], y[1];
-        if (V == 4) {
+        if (V >= 4) {
             PolarCand c[1];
             bool ok;
             do {
@@ -389,7 +393,10 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
                 used += 2;
                 ok = polar_candidate(wa, wb, c[0]);
             } while (!ok);
-            polar_transform<1>(c, p.tp, tab, x, y);
+            if (V == 5)
+                p2_transform<1>(c, p.tp, tab, x, y);
+            else
+                polar_transform<1>(c, p.tp, tab, x, y);
         } else if (V == 3) {
             const uint64_t w1[1] = {rc.next()}, w2[1] = {rc.next()}, w3[1] = {rc.next()};
             used += 3;
@@ -493,7 +500,12 @@ __global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs,
             PolarCand pc[1];
             const bool ok = polar_candidate(word_of(u[2 * j]), word_of(u[2 * j + 1]), pc[0]);
             if (mask) mask[j] = ok ? 1 : 0;
-            if (ok) polar_transform<1>(pc, tp, tab, x, y);
+            if (ok) {
+                if (method == 5)
+                    p2_transform<1>(pc, tp, tab, x, y);
+                else
+                    polar_transform<1>(pc, tp, tab, x, y);
+            }
         }
         out[2 * j] = x[0];
         out[2 * j + 1] = y[0];

@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "nrng.h")
 def declared_functions():
     txt = open(HEADER).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(nrng_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(nrng_[a-z0-9_]+)\s*\(", txt)))
 
 
 @pytest.fixture(scope="module")
@@ -35,7 +35,7 @@ def test_every_declared_symbol_is_exported(libnrng):
     for name in declared_functions():
         assert hasattr(L, name), name
     nm = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
-    exported = set(re.findall(r"\bT (nrng_[a-z_]+)", nm))
+    exported = set(re.findall(r"\bT (nrng_[a-z0-9_]+)", nm))
     assert set(declared_functions()) <= exported
 
 

@@ -44,11 +44,38 @@ def gen_normals(g, method, n, mu, sigma):
 def ora_normals(st, method, n, mu, sigma):
     if method == "P":
         return st.normal_polar(n, mu, sigma)
+    if method == "P2":
+        return st.normal_polar2(n, mu, sigma)
     return st.normal_boxmuller(n, mu, sigma, P.METHODS[method])
 
 
 def tol_for(method):
     return TOL if method in ("B1", "P") else TOL_APPROX
+
+
+def test_c2_polar2_full():
+    # method P2 on config 2's shape: same candidates as P
+    c = W.C2
+    g, st = P.Generator(c.seed, c.streams), O.Streams(c.seed, c.streams)
+    d = gen_normals(g, "P2", c.n, 2.5, 0.5)
+    o = ora_normals(st, "P2", c.n, 2.5, 0.5)
+    assert np.max(np.abs(d - o)) <= TOL_APPROX
+    assert_state_equal(g, st)
+
+
+def test_p2_shard_sampled():
+    c = W.C5_SHARD
+    g = P.Generator(c.seed, c.streams)
+    out = torch.empty(c.n, dtype=torch.float64, device="cuda")
+    g.normal("P2", out=out)
+    per_stream = c.n // c.streams
+    counts = g.stream_counts()
+    for k in (0, 777, c.streams - 1):
+        st = O.Streams(c.seed, 1, first_stream=k)
+        o = st.normal_polar2(per_stream)
+        assert np.max(np.abs(host(out[k * per_stream:(k + 1) * per_stream]) - o)) <= TOL_APPROX
+        assert counts[k] == st.counts[0]
+    del out
 
 
 def assert_state_equal(g, st):
@@ -168,7 +195,7 @@ def test_c4_sweep_sequence():
 
 # ---------------------------------------------------------------- transforms on given uniforms
 
-@pytest.mark.parametrize("method", [1, 2, 3, 4])
+@pytest.mark.parametrize("method", [1, 2, 3, 4, 5])
 def test_transform_from_uniforms(method):
     per = 3 if method == 3 else 2
     u = W.dyadic_uniforms(100 + method, per * 300001)
@@ -180,7 +207,7 @@ def test_transform_from_uniforms(method):
     d_out, d_mask = P.transform_from_uniforms(torch.from_numpy(u).cuda(), method, mu, sigma)
     o_out, o_mask = O.transform_from_uniforms(u, method, mu, sigma)
     d_out = host(d_out)
-    if method == 4:
+    if method >= 4:
         assert np.array_equal(host(d_mask), o_mask)
         acc = np.repeat(o_mask.astype(bool), 2)
         assert np.all(np.isnan(d_out[~acc]))
@@ -190,6 +217,13 @@ def test_transform_from_uniforms(method):
         # the bulk branch (u <= 8/9) has no library call: bit-exact
         m = np.maximum(u[0::3], u[1::3])
         bulk = np.repeat(m * m <= 8 / 9, 2)
+        assert np.array_equal(d_out[bulk], o_out[bulk])
+    if method == 5:
+        # P2's bulk branch (s <= 8/9): bit-exact
+        x, y = 2 * u[0::2] - 1, 2 * u[1::2] - 1
+        s = x * x + y * y
+        acc = s < 1
+        bulk = np.repeat(s[acc] <= 8 / 9, 2)
         assert np.array_equal(d_out[bulk], o_out[bulk])
 
 
@@ -208,7 +242,7 @@ def test_zero_n_is_noop_and_sigma_zero():
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 63, 64, 65, 127, 129, 2 * 64 * 4 + 1, 2 * 64 * 5 - 1, 2 * 64 * 33 + 1])
-@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P"])
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P", "P2"])
 def test_small_and_odd_n(n, method):
     # n <= 2 * 64 * 4: one thread per stream (tiny quotas); larger: warp per stream
     S = 64
