@@ -345,6 +345,83 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
     }
 }
 
+// Direct variant: the survivors are compacted only in the OUTPUT -- each accepted
+// candidate's pair index is its __ballot_sync/__popc rank in candidate order -- and the
+// warp transforms all 64 candidates of a step, rejected lanes predicated off at the
+// store.  On the VP2200 the compress made vector lengths full; on a GPU the
+// 21.5% of lanes that do wasted work cost less than a queue's per-candidate bookkeeping.
+template <int NW, int M>
+__global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_direct_kernel(BulkParams p) {
+    extern __shared__ __align__(16) uint64_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
+    __syncthreads();
+    WarpLFG L;
+    L.buf = smem + warp * kWinAlloc;
+    const unsigned lt = lanemask_lt(lane);
+    for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
+        const Quota qk = quota(p.q, p.rem, k);
+        if (qk.cnt == 0) continue;
+        const uint64_t C = p.count[k];
+        uint64_t* rk = p.ring + (uint64_t)k * kPitch;
+        lfg_load(L, rk, C, lane);
+        const bool fast = p.aligned && 2 * (qk.off + qk.cnt) <= p.n;
+        for (uint64_t base = 0; base < qk.cnt;) {
+            const uint32_t cnt = (uint32_t)(qk.cnt - base < (1ull << 31) ? qk.cnt - base : (1ull << 31));
+            double2* o = reinterpret_cast<double2*>(p.out + (2 * (qk.off + base) - p.shift));
+            uint32_t acc = 0;  // accepted pairs of this chunk
+            while (acc < cnt) {
+                lfg_ensure(L, lane, 128);
+                const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(L.at(2 * lane));
+                const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(L.at(64 + 2 * lane));
+                PolarCand c[2];
+                const bool ok0 = polar_candidate(w0.x, w0.y, c[0]);
+                const bool ok1 = polar_candidate(w1.x, w1.y, c[1]);
+                unsigned m0 = __ballot_sync(kFull, ok0), m1 = __ballot_sync(kFull, ok1);
+                const uint32_t need = cnt - acc;
+                uint32_t used = 64;
+                if ((uint32_t)(__popc(m0) + __popc(m1)) >= need) {
+                    if ((uint32_t)__popc(m0) >= need) {
+                        const unsigned last = __ballot_sync(kFull, ok0 && (uint32_t)__popc(m0 & lt) == need - 1);
+                        const int l = __ffs(last) - 1;
+                        m0 &= (l == 31) ? kFull : ((2u << l) - 1u);
+                        m1 = 0;
+                        used = l + 1;
+                    } else {
+                        const uint32_t need1 = need - __popc(m0);
+                        const unsigned last = __ballot_sync(kFull, ok1 && (uint32_t)__popc(m1 & lt) == need1 - 1);
+                        const int l = __ffs(last) - 1;
+                        m1 &= (l == 31) ? kFull : ((2u << l) - 1u);
+                        used = 32 + l + 1;
+                    }
+                }
+                const uint32_t n0 = __popc(m0);
+                const uint32_t j0 = acc + __popc(m0 & lt), j1 = acc + n0 + __popc(m1 & lt);
+                double ox[2], oy[2];
+                if (M == 2)
+                    p2_transform<2>(c, p.tp, tab, ox, oy);
+                else
+                    polar_transform<2>(c, p.tp, tab, ox, oy);
+                const bool k0 = (m0 >> lane) & 1u, k1 = (m1 >> lane) & 1u;
+                if (fast) {
+                    if (k0) __stcs(o + j0, make_double2(ox[0], oy[0]));
+                    if (k1) __stcs(o + j1, make_double2(ox[1], oy[1]));
+                } else {
+                    if (k0) store_pair(p.out, 2 * (qk.off + base + j0), p.shift, p.n, ox[0], oy[0], p.aligned);
+                    if (k1) store_pair(p.out, 2 * (qk.off + base + j1), p.shift, p.n, ox[1], oy[1], p.aligned);
+                }
+                acc += n0 + __popc(m1);
+                L.wc += 2 * used;
+                __syncwarp();
+            }
+            base += cnt;
+        }
+        lfg_store(L, rk, C, lane);
+        if (lane == 0) p.count[k] = C + (L.wc - kW0);
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------------------ tiny quotas
 // Calls that give every stream only a few pairs (the C4 sweep: n <= 2^18 over 2^16
 // streams) are bound by per-stream latency and state traffic, not arithmetic: one THREAD
