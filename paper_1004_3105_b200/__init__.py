@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libnrng.so")
+LIB_PATH = os.environ.get("NRNG_LIB_OVERRIDE") or os.path.join(PKG, "libnrng.so")  # override: A/B builds only
 
 NRNG_DEFAULT, NRNG_B1, NRNG_B2, NRNG_B3, NRNG_POLAR, NRNG_POLAR2 = 0, 1, 2, 3, 4, 5
 NRNG_OK, NRNG_EINVAL, NRNG_ENOMEM, NRNG_ECUDA, NRNG_ENODEV = 0, -1, -2, -3, -4

@@ -33,9 +33,8 @@ int cuda_err(cudaError_t e) {
     return set_err(NRNG_ECUDA);
 }
 
-constexpr size_t bm_smem(int nw) { return win_bytes(nw) + kTabBytes + tailq_bytes(nw); }
-constexpr size_t polar_smem(int nw) { return win_bytes(nw) + kTabBytes + queue_bytes(nw); }
-constexpr size_t bm_smem_notail(int nw) { return win_bytes(nw) + kTabBytes; }
+constexpr size_t bm_smem(int nw) { return win_bytes(nw) + kTabBytes; }
+constexpr size_t polar_smem(int nw) { return win_bytes(nw) + kTabBytes; }
 constexpr size_t kUniSmem = win_bytes(kWarpsPerBlock);
 constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
 constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)
@@ -102,16 +101,6 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
 
 template <int M>
 void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
-    static const bool queued = getenv("NRNG_POLAR_QUEUE") != nullptr;  // A/B switch (profiling)
-    if (!queued) {
-        if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
-            polar_direct_kernel<kBigBlockPolar, M>
-                <<<h->num_sms, kBigBlockPolar * 32, bm_smem_notail(kBigBlockPolar), st>>>(p);
-        else
-            polar_direct_kernel<kWarpsPerBlock, M><<<grid_for(ns, kWarpsPerBlock, h->occ.polar, h->num_sms),
-                                                     kWarpsPerBlock * 32, bm_smem_notail(kWarpsPerBlock), st>>>(p);
-        return;
-    }
     if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
         polar_kernel<kBigBlockPolar, M><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
     else
@@ -260,10 +249,6 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(bm_kernel<3, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     occupancy(polar_kernel<kBigBlockPolar, 2>, kBigBlockPolar, polar_smem(kBigBlockPolar));
-    occupancy(polar_direct_kernel<kBigBlockPolar, 1>, kBigBlockPolar, bm_smem_notail(kBigBlockPolar));
-    occupancy(polar_direct_kernel<kBigBlockPolar, 2>, kBigBlockPolar, bm_smem_notail(kBigBlockPolar));
-    occupancy(polar_direct_kernel<kWarpsPerBlock, 1>, kWarpsPerBlock, bm_smem_notail(kWarpsPerBlock));
-    occupancy(polar_direct_kernel<kWarpsPerBlock, 2>, kWarpsPerBlock, bm_smem_notail(kWarpsPerBlock));
     h->occ.uni = occupancy(uniform_kernel, kWarpsPerBlock, kUniSmem);
     h->occ.mask = occupancy(polar_mask_kernel, kWarpsPerBlock, kUniSmem);
     h->occ.init = occupancy(init_kernel, kWarpsPerBlock, kInitSmem);

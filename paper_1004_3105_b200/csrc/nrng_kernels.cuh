@@ -102,35 +102,6 @@ __device__ __forceinline__ void bm_pairs(const uint64_t* src, const TParams& tp,
     }
 }
 
-// B3 tail compaction (fast path only).  A pair with u > tau (prob. 1/9) needs ln + sqrt
-// instead of the Moebius/Horner bulk path; evaluating both for every lane would cost the
-// tail's ~33 instructions on every pair.  Instead the bulk pass leaves (c, s) in the tail
-// pair's output slot and appends the local index of its first word to a per-warp list;
-// every kTailEvery iterations (before those words can leave the window: the window keeps
-// >= 1024 - 319 words of history) the list is drained 32 entries per warp step: re-read
-// u1, u2 from the window, compute the radius, read back (c, s), write the final pair.
-constexpr int kTailEvery = 3;
-constexpr int kTailCap = kTailEvery * 64;  // entries per drain (U = 2: <= 64 per iteration)
-constexpr int kTailAlloc = kTailCap + 32;   // + one scratch slot per lane (branch-free append)
-constexpr size_t tailq_bytes(int nw) { return (size_t)nw * kTailAlloc * sizeof(uint32_t); }
-
-__device__ __forceinline__ void b3_tail_drain(const uint32_t* tq, uint32_t tn, const uint64_t* buf, double2* o0,
-                                              int lane, const TParams& tp, const Tables& tab) {
-    for (uint32_t base = 0; base < tn; base += 32) {
-        const bool act = base + lane < tn;
-        const uint32_t wl = act ? tq[base + lane] : kW0;
-        const uint64_t* src = buf + (wl & kWinMask);
-        const uint64_t k1 = ukey(src[0]), k2 = ukey(src[1]);
-        const uint64_t Mk[1] = {k1 > k2 ? k1 : k2};
-        const uint32_t j = (wl - kW0) / 3;
-        const double2 cs = act ? o0[j] : make_double2(0.0, 0.0);
-        const double c[1] = {cs.x}, s[1] = {cs.y};
-        double x[1], y[1];
-        b3_tail_finish<1>(Mk, c, s, tp, tab, x, y);
-        if (act) __stcs(o0 + j, make_double2(x[0], y[0]));
-    }
-}
-
 template <int V, int NW>
 __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
@@ -145,7 +116,6 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
     __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
-    uint32_t* tq = reinterpret_cast<uint32_t*>(smem + NW * kWinAlloc + kTabBytes / 8) + warp * kTailAlloc;
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
@@ -153,53 +123,16 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         lfg_load(L, rk, C, lane, qk.cnt * per < (uint64_t)kLagR ? (uint32_t)(qk.cnt * per) : (uint32_t)kLagR);
         uint64_t j0 = 0;
-        if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n && (V != 3 || qk.cnt * per < (1ull << 31))) {
-            double2* o0 = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift));
-            double2* o = o0 + lane;
+        if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
+            double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
             const uint64_t full = qk.cnt - qk.cnt % (32 * kU);
-            uint32_t tn = 0, it = 0;  // B3: queued tail pairs, iterations since the last drain
             for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
                 lfg_ensure<kB>(L, lane, kNeedU);
-                const uint64_t* src = L.at(per * lane);
                 double x[kU], y[kU];
-                if (V == 3) {
-                    uint64_t w1[kU], w2[kU], w3[kU], Mk[kU];
-                    bool tail[kU];
+                bm_pairs<V, kU>(L.at(per * lane), p.tp, tab, x, y);
 #pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        w1[u] = src[32 * per * u];
-                        w2[u] = src[32 * per * u + 1];
-                        w3[u] = src[32 * per * u + 2];
-                    }
-                    b3_bulk<kU>(w1, w2, w3, p.tp, x, y, tail, Mk);
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
-                    // branch-free append of the tail pairs' first-word local indices
-                    const uint32_t wl = L.wc + per * lane;
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        const unsigned m = __ballot_sync(kFull, tail[u]);
-                        const uint32_t slot = tail[u] ? tn + __popc(m & lanemask_lt(lane)) : kTailCap + lane;
-                        tq[slot] = wl + 32 * per * u;
-                        tn += __popc(m);
-                    }
-                    if (++it == kTailEvery) {
-                        __syncwarp();
-                        b3_tail_drain(tq, tn, L.buf, o0, lane, p.tp, tab);
-                        tn = 0;
-                        it = 0;
-                    }
-                } else {
-                    bm_pairs<V, kU>(src, p.tp, tab, x, y);
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
-                }
+                for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
                 L.wc += kNeedU;
-                __syncwarp();
-            }
-            if (V == 3 && tn > 0) {
-                __syncwarp();
-                b3_tail_drain(tq, tn, L.buf, o0, lane, p.tp, tab);
                 __syncwarp();
             }
         }
@@ -222,136 +155,26 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
 }
 
 // ------------------------------------------------------------------ Polar P
-// Candidate phase: 64 candidates (128 uniforms) per warp step, two per lane: candidate i
-// of the step is lane i%32's (i < 32: words wc + 2i, i >= 32: wc + 64 + 2(i-32)).  Accepts
-// are ranked with __ballot_sync/__popc in candidate order, trimmed at the stream's
-// remaining quota (exact stop, R5: the last step consumes candidates only up to the
-// p_k-th accept), and the window position of each survivor is appended to a per-warp
-// shared-memory queue (4 bytes per entry: the words stay in the window, which keeps >= 600
-// words of history behind wc).  Transform phase: whenever >= 64 survivors are queued the
-// warp re-reads their words, recomputes (X, Y, S) and transforms 64 of them densely (two
-// per lane; no lane idles on a rejected candidate), storing 64 consecutive pairs.
-constexpr int kQueue = 128;
-constexpr int kQueueAlloc = kQueue + 32;  // ring + one scratch slot per lane
-constexpr size_t queue_bytes(int nw) { return (size_t)nw * kQueueAlloc * sizeof(uint32_t); }
-
-template <int U, int M>
-__device__ __forceinline__ void polar_from_queue(const uint64_t* buf, const uint32_t* q, uint32_t first, int lane,
-                                                 const TParams& tp, const Tables& tab, double (&ox)[U],
-                                                 double (&oy)[U]) {
-    PolarCand c[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(buf + q[(first + 32 * u + lane) & (kQueue - 1)]);
-        polar_candidate(w.x, w.y, c[u]);
-    }
-    if (M == 2)
-        p2_transform<U>(c, tp, tab, ox, oy);
-    else
-        polar_transform<U>(c, tp, tab, ox, oy);
-}
-
+// 64 candidates (128 uniforms) per warp step, two per lane: candidate i of the step is
+// lane i%32's (i < 32: words wc + 2i, i >= 32: wc + 64 + 2(i-32)).  Accepts are ranked
+// with __ballot_sync/__popc in candidate order and trimmed at the stream's remaining quota
+// (exact stop, R5: the last step consumes candidates only up to the p_k-th accept); each
+// survivor's rank is its pair index, so the output is stream-major then accepted-pair
+// order with no gaps.
+// The survivors are compacted in the OUTPUT only: the warp transforms all 64 candidates
+// of a step and rejected lanes are predicated off at the store.  On the VP2200 the
+// compress made vector lengths full; on a GPU the 21.5% of lanes doing wasted
+// work cost less than a survivor queue's per-candidate bookkeeping (measured: a shared-
+// memory queue with dense 64-wide transforms ran 6.4 ms vs 5.7 ms per 2^31 normals).
 // M = 1: Algorithm P (= the paper's P1); M = 2: method P2, same candidates.
+#ifndef NRNG_POLAR_U
+#define NRNG_POLAR_U 4
+#endif
+constexpr int kPU = NRNG_POLAR_U;  // candidates per lane per step (32 kPU per warp)
+constexpr int kPB = 128; // refill batch: lookahead 64 kPU - 1 + kPB <= 417
+static_assert(64 * kPU - 1 + kPB <= kWin - kLagR && 64 * kPU <= kMirror, "polar window bounds");
 template <int NW, int M>
 __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_kernel(BulkParams p) {
-    extern __shared__ __align__(16) uint64_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
-    __syncthreads();
-    WarpLFG L;
-    L.buf = smem + warp * kWinAlloc;
-    uint32_t* q = reinterpret_cast<uint32_t*>(smem + NW * kWinAlloc + kTabBytes / 8) + warp * kQueueAlloc;
-    const unsigned lt = lanemask_lt(lane);
-    for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
-        const Quota qk = quota(p.q, p.rem, k);
-        if (qk.cnt == 0) continue;
-        const uint64_t C = p.count[k];
-        uint64_t* rk = p.ring + (uint64_t)k * kPitch;
-        lfg_load(L, rk, C, lane);
-        const bool fast = p.aligned && 2 * (qk.off + qk.cnt) <= p.n;
-        // the stream's quota in chunks of < 2^31 pairs: 32-bit counters in the loops
-        for (uint64_t base = 0; base < qk.cnt;) {
-            const uint32_t cnt = (uint32_t)(qk.cnt - base < (1ull << 31) ? qk.cnt - base : (1ull << 31));
-            double2* o = reinterpret_cast<double2*>(p.out + (2 * (qk.off + base) - p.shift)) + lane;
-            uint32_t acc = 0;   // accepted (queued) pairs of this chunk
-            uint32_t done = 0;  // pairs transformed and stored
-            while (acc < cnt) {
-                lfg_ensure(L, lane, 128);
-                const uint32_t pos0 = (L.wc & kWinMask) + 2 * lane, pos1 = pos0 + 64;
-                const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(L.buf + pos0);
-                const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(L.buf + pos1);
-                PolarCand c0, c1;
-                const bool ok0 = polar_candidate(w0.x, w0.y, c0);
-                const bool ok1 = polar_candidate(w1.x, w1.y, c1);
-                unsigned m0 = __ballot_sync(kFull, ok0), m1 = __ballot_sync(kFull, ok1);
-                const uint32_t need = cnt - acc;
-                uint32_t used = 64;
-                if ((uint32_t)(__popc(m0) + __popc(m1)) >= need) {
-                    // exact stop: keep the first `need` accepts in candidate order
-                    if ((uint32_t)__popc(m0) >= need) {
-                        const unsigned last = __ballot_sync(kFull, ok0 && (uint32_t)__popc(m0 & lt) == need - 1);
-                        const int l = __ffs(last) - 1;
-                        m0 &= (l == 31) ? kFull : ((2u << l) - 1u);
-                        m1 = 0;
-                        used = l + 1;
-                    } else {
-                        const uint32_t need1 = need - __popc(m0);
-                        const unsigned last = __ballot_sync(kFull, ok1 && (uint32_t)__popc(m1 & lt) == need1 - 1);
-                        const int l = __ffs(last) - 1;
-                        m1 &= (l == 31) ? kFull : ((2u << l) - 1u);
-                        used = 32 + l + 1;
-                    }
-                }
-                // branch-free append: rejected lanes write their position to a per-lane
-                // scratch slot past the ring (q[kQueue + lane]) instead of skipping the store
-                const uint32_t n0 = __popc(m0);
-                const uint32_t s0 = ((m0 >> lane) & 1u) ? ((acc + __popc(m0 & lt)) & (kQueue - 1)) : kQueue + lane;
-                const uint32_t s1 =
-                    ((m1 >> lane) & 1u) ? ((acc + n0 + __popc(m1 & lt)) & (kQueue - 1)) : kQueue + lane;
-                q[s0] = pos0;
-                q[s1] = pos1;
-                acc += n0 + __popc(m1);
-                L.wc += 2 * used;
-                __syncwarp();
-                if (fast && acc - done >= 64) {
-                    double ox[2], oy[2];
-                    polar_from_queue<2, M>(L.buf, q, done, lane, p.tp, tab, ox, oy);
-                    __stcs(o + done, make_double2(ox[0], oy[0]));
-                    __stcs(o + done + 32, make_double2(ox[1], oy[1]));
-                    done += 64;
-                    __syncwarp();
-                }
-                while (!fast && acc - done >= 32) {
-                    double ox[1], oy[1];
-                    polar_from_queue<1, M>(L.buf, q, done, lane, p.tp, tab, ox, oy);
-                    store_pair(p.out, 2 * (qk.off + base + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
-                    done += 32;
-                    __syncwarp();
-                }
-            }
-            for (; done < acc; done += 32) {
-                if ((uint32_t)lane < acc - done) {
-                    double ox[1], oy[1];
-                    polar_from_queue<1, M>(L.buf, q, done, lane, p.tp, tab, ox, oy);
-                    store_pair(p.out, 2 * (qk.off + base + done + lane), p.shift, p.n, ox[0], oy[0], p.aligned);
-                }
-                __syncwarp();
-            }
-            base += cnt;
-        }
-        lfg_store(L, rk, C, lane);
-        if (lane == 0) p.count[k] = C + (L.wc - kW0);
-        __syncwarp();
-    }
-}
-
-// Direct variant: the survivors are compacted only in the OUTPUT -- each accepted
-// candidate's pair index is its __ballot_sync/__popc rank in candidate order -- and the
-// warp transforms all 64 candidates of a step, rejected lanes predicated off at the
-// store.  On the VP2200 the compress made vector lengths full; on a GPU the
-// 21.5% of lanes that do wasted work cost less than a queue's per-candidate bookkeeping.
-template <int NW, int M>
-__global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_direct_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
@@ -371,46 +194,58 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_d
             double2* o = reinterpret_cast<double2*>(p.out + (2 * (qk.off + base) - p.shift));
             uint32_t acc = 0;  // accepted pairs of this chunk
             while (acc < cnt) {
-                lfg_ensure(L, lane, 128);
-                const ulonglong2 w0 = *reinterpret_cast<const ulonglong2*>(L.at(2 * lane));
-                const ulonglong2 w1 = *reinterpret_cast<const ulonglong2*>(L.at(64 + 2 * lane));
-                PolarCand c[2];
-                const bool ok0 = polar_candidate(w0.x, w0.y, c[0]);
-                const bool ok1 = polar_candidate(w1.x, w1.y, c[1]);
-                unsigned m0 = __ballot_sync(kFull, ok0), m1 = __ballot_sync(kFull, ok1);
-                const uint32_t need = cnt - acc;
-                uint32_t used = 64;
-                if ((uint32_t)(__popc(m0) + __popc(m1)) >= need) {
-                    if ((uint32_t)__popc(m0) >= need) {
-                        const unsigned last = __ballot_sync(kFull, ok0 && (uint32_t)__popc(m0 & lt) == need - 1);
-                        const int l = __ffs(last) - 1;
-                        m0 &= (l == 31) ? kFull : ((2u << l) - 1u);
-                        m1 = 0;
-                        used = l + 1;
-                    } else {
-                        const uint32_t need1 = need - __popc(m0);
-                        const unsigned last = __ballot_sync(kFull, ok1 && (uint32_t)__popc(m1 & lt) == need1 - 1);
-                        const int l = __ffs(last) - 1;
-                        m1 &= (l == 31) ? kFull : ((2u << l) - 1u);
-                        used = 32 + l + 1;
+                lfg_ensure<kPB>(L, lane, 64 * kPU);
+                PolarCand c[kPU];
+                bool ok[kPU];
+                unsigned m[kPU];
+#pragma unroll
+                for (int u = 0; u < kPU; ++u) {
+                    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(L.at(64 * u + 2 * lane));
+                    ok[u] = polar_candidate(w.x, w.y, c[u]);
+                }
+                uint32_t tot = 0;
+#pragma unroll
+                for (int u = 0; u < kPU; ++u) {
+                    m[u] = __ballot_sync(kFull, ok[u]);
+                    tot += __popc(m[u]);
+                }
+                uint32_t used = 32 * kPU;
+                if (tot >= cnt - acc) {  // exact stop: keep the first `need` accepts in candidate order
+                    uint32_t rem = cnt - acc;
+#pragma unroll
+                    for (int u = 0; u < kPU; ++u) {
+                        const uint32_t nu = __popc(m[u]);
+                        if (rem == 0) {
+                            m[u] = 0;
+                        } else if (nu >= rem) {
+                            const unsigned last = __ballot_sync(kFull, ok[u] && (uint32_t)__popc(m[u] & lt) == rem - 1);
+                            const int l = __ffs(last) - 1;
+                            m[u] &= (l == 31) ? kFull : ((2u << l) - 1u);
+                            used = 32 * u + l + 1;
+                            rem = 0;
+                        } else {
+                            rem -= nu;
+                        }
                     }
                 }
-                const uint32_t n0 = __popc(m0);
-                const uint32_t j0 = acc + __popc(m0 & lt), j1 = acc + n0 + __popc(m1 & lt);
-                double ox[2], oy[2];
+                double ox[kPU], oy[kPU];
                 if (M == 2)
-                    p2_transform<2>(c, p.tp, tab, ox, oy);
+                    p2_transform<kPU>(c, p.tp, tab, ox, oy);
                 else
-                    polar_transform<2>(c, p.tp, tab, ox, oy);
-                const bool k0 = (m0 >> lane) & 1u, k1 = (m1 >> lane) & 1u;
-                if (fast) {
-                    if (k0) __stcs(o + j0, make_double2(ox[0], oy[0]));
-                    if (k1) __stcs(o + j1, make_double2(ox[1], oy[1]));
-                } else {
-                    if (k0) store_pair(p.out, 2 * (qk.off + base + j0), p.shift, p.n, ox[0], oy[0], p.aligned);
-                    if (k1) store_pair(p.out, 2 * (qk.off + base + j1), p.shift, p.n, ox[1], oy[1], p.aligned);
+                    polar_transform<kPU>(c, p.tp, tab, ox, oy);
+                uint32_t j = acc;
+#pragma unroll
+                for (int u = 0; u < kPU; ++u) {
+                    const uint32_t ju = j + __popc(m[u] & lt);
+                    if ((m[u] >> lane) & 1u) {
+                        if (fast)
+                            __stcs(o + ju, make_double2(ox[u], oy[u]));
+                        else
+                            store_pair(p.out, 2 * (qk.off + base + ju), p.shift, p.n, ox[u], oy[u], p.aligned);
+                    }
+                    j += __popc(m[u]);
                 }
-                acc += n0 + __popc(m1);
+                acc = j;
                 L.wc += 2 * used;
                 __syncwarp();
             }
