@@ -99,6 +99,24 @@ int nrng_normal_polar(nrng_handle h, double* out, size_t n, double mu, double si
  * y r sqrt2 + mu.  Errors as nrng_normal_polar. */
 int nrng_normal_polar2(nrng_handle h, double* out, size_t n, double mu, double sigma);
 
+/* ---- sequential mode: RANN3-style buffering ----
+ * One canonical, partition-invariant sequence per handle and method: epoch e is the output
+ * of every stream making E more pairs, stream-major (2 S E deviates; E = epoch_pairs, a
+ * power of two in [128, 2^20], default 128).  nrng_normal_seq(h, out, n, ...) returns the
+ * next n deviates of that sequence: it first drains the deviates left over from the last
+ * partially used epoch (kept in a handle-owned device buffer of 2 S E doubles), then writes
+ * whole epochs straight into `out` (one launch), then generates one more epoch into the
+ * buffer for the remainder.  Any split of a total into calls gives the same concatenated
+ * output; odd counts and Polar's exact-count requirement need no dropped deviates.
+ * EINVAL if deviates of another (method, mu, sigma) are still buffered (nrng_seq_reset
+ * discards them; their uniforms stay consumed).  method: 1/2/3 = B1/B2/B3, 4 = P, 5 = P2.
+ * out: device or host pointer, as for the bulk calls.  The state checkpoint
+ * (nrng_get_state) does not include the buffer: reset or drain before checkpointing. */
+int nrng_seq_configure(nrng_handle h, uint32_t epoch_pairs);
+int nrng_normal_seq(nrng_handle h, double* out, size_t n, double mu, double sigma, int method);
+size_t nrng_seq_buffered(nrng_handle h);
+int nrng_seq_reset(nrng_handle h);
+
 /* Thread-local status of the last nrng_* call on this thread, and its text. */
 int nrng_last_error(void);
 const char* nrng_error_string(int code);

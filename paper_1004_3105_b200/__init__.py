@@ -33,6 +33,10 @@ SIGNATURES = {
     "nrng_normal_boxmuller": ([_p, _p, _sz, _dbl, _dbl, _int], _int),
     "nrng_normal_polar": ([_p, _p, _sz, _dbl, _dbl], _int),
     "nrng_normal_polar2": ([_p, _p, _sz, _dbl, _dbl], _int),
+    "nrng_seq_configure": ([_p, _u32], _int),
+    "nrng_normal_seq": ([_p, _p, _sz, _dbl, _dbl, _int], _int),
+    "nrng_seq_buffered": ([_p], _sz),
+    "nrng_seq_reset": ([_p], _int),
     "nrng_last_error": ([], _int),
     "nrng_error_string": ([_int], C.c_char_p),
     "nrng_num_streams": ([_p], _u32),
@@ -118,6 +122,22 @@ def nrng_normal_polar(h, out_ptr: int, n: int, mu: float, sigma: float) -> None:
 
 def nrng_normal_polar2(h, out_ptr: int, n: int, mu: float, sigma: float) -> None:
     _check(lib().nrng_normal_polar2(h, out_ptr, n, mu, sigma), "nrng_normal_polar2")
+
+
+def nrng_seq_configure(h, epoch_pairs: int) -> None:
+    _check(lib().nrng_seq_configure(h, epoch_pairs), "nrng_seq_configure")
+
+
+def nrng_normal_seq(h, out_ptr: int, n: int, mu: float, sigma: float, method: int) -> None:
+    _check(lib().nrng_normal_seq(h, out_ptr, n, mu, sigma, method), "nrng_normal_seq")
+
+
+def nrng_seq_buffered(h) -> int:
+    return int(lib().nrng_seq_buffered(h))
+
+
+def nrng_seq_reset(h) -> None:
+    _check(lib().nrng_seq_reset(h), "nrng_seq_reset")
 
 
 def nrng_uniform(h, out_ptr: int, n: int) -> None:
@@ -254,6 +274,13 @@ class Generator:
         if method == "P2":
             return self.normal_polar2(n, mu, sigma, out=out)
         return self.normal_boxmuller(n, mu, sigma, METHODS[method], out=out)
+
+    def normal_seq(self, method: str, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
+        """Next n deviates of the handle's canonical sequence (RANN3-style buffering)."""
+        out, ptr, n = self._out(n, out)
+        self._sync_stream()
+        nrng_normal_seq(self.h, ptr, n, mu, sigma, METHODS[method])
+        return out
 
     def uniform(self, n: int = None, out=None):
         out, ptr, n = self._out(n, out)

@@ -60,6 +60,14 @@ struct nrng_gen {
     cudaEvent_t ev_free[2] = {nullptr, nullptr};
     uint64_t launches = 0;
     Occ occ;
+    // sequential (RANN3-style) mode: the partially consumed last epoch
+    struct {
+        double* buf = nullptr;
+        uint32_t log2E = 7;  // E = 128 pairs per stream per epoch
+        uint64_t len = 0, pos = 0;
+        int method = 0;
+        double mu = 0, sigma = 0;
+    } seq;
 };
 
 namespace {
@@ -300,6 +308,7 @@ void nrng_destroy(nrng_handle h) {
         if (h->ev_ready[i]) cudaEventDestroy(h->ev_ready[i]);
         if (h->ev_free[i]) cudaEventDestroy(h->ev_free[i]);
     }
+    cudaFree(h->seq.buf);
     cudaFree(h->ring);
     cudaFree(h->count);
     delete h;
@@ -333,6 +342,101 @@ int nrng_normal_polar2(nrng_handle h, double* out, size_t n, double mu, double s
     if (!check_device(h)) return set_err(NRNG_EINVAL);
     if (n == 0) return set_err(NRNG_OK);
     return run_bulk(h, Kind::POLAR2, out, n, (n + 1) / 2, 2, mu, sigma);
+}
+
+// ---------------------------------------------------------------- sequential mode
+namespace {
+Kind kind_of(int method) {
+    return method == 1 ? Kind::BM1 : method == 2 ? Kind::BM2 : method == 3 ? Kind::BM3
+         : method == 4 ? Kind::POLAR : Kind::POLAR2;
+}
+// `epochs` whole epochs into device memory dst (epoch layout).
+int seq_epochs(nrng_handle h, int method, double* dst, uint64_t epochs, double mu, double sigma) {
+    BulkParams p{};
+    p.ring = h->ring;
+    p.count = h->count;
+    p.q = epochs << h->seq.log2E;
+    p.rem = 0;
+    p.units = p.q * h->S;
+    p.n = 2 * p.units;
+    p.tp = TParams{mu, sigma, 2.0 * sigma};
+    p.out = dst;
+    p.shift = 0;
+    p.aligned = ((uintptr_t)dst & 15) == 0;
+    p.s_begin = 0;
+    p.s_end = h->S;
+    p.log2E = h->seq.log2E;
+    p.S = h->S;
+    return cuda_err(launch_bulk(h, kind_of(method), p, h->stream));
+}
+}  // namespace
+
+int nrng_seq_configure(nrng_handle h, uint32_t epoch_pairs) {
+    if (!h || epoch_pairs < 128 || epoch_pairs > (1u << 20) || (epoch_pairs & (epoch_pairs - 1)))
+        return set_err(NRNG_EINVAL);
+    cudaStreamSynchronize(h->stream);
+    cudaFree(h->seq.buf);
+    h->seq.buf = nullptr;
+    h->seq.log2E = 31 - __builtin_clz(epoch_pairs);
+    h->seq.len = h->seq.pos = 0;
+    return set_err(NRNG_OK);
+}
+
+int nrng_seq_reset(nrng_handle h) {
+    if (!h) return set_err(NRNG_EINVAL);
+    h->seq.len = h->seq.pos = 0;
+    return set_err(NRNG_OK);
+}
+
+size_t nrng_seq_buffered(nrng_handle h) { return h ? (size_t)(h->seq.len - h->seq.pos) : 0; }
+
+int nrng_normal_seq(nrng_handle h, double* out, size_t n, double mu, double sigma, int method) {
+    if (!h || (n > 0 && !out) || bad_params(mu, sigma) || method < 1 || method > 5) return set_err(NRNG_EINVAL);
+    if (!check_device(h)) return set_err(NRNG_EINVAL);
+    auto& q = h->seq;
+    if (q.pos < q.len && (q.method != method || q.mu != mu || q.sigma != sigma)) return set_err(NRNG_EINVAL);
+    if (n == 0) return set_err(NRNG_OK);
+    const uint64_t epoch = 2ull * h->S << q.log2E;  // deviates per epoch
+    if (!q.buf && cudaMalloc(&q.buf, epoch * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(NRNG_ENOMEM);
+    }
+    cudaError_t e = cudaSuccess;
+    uint64_t done = std::min<uint64_t>(n, q.len - q.pos);
+    // whole epochs go straight into device outputs that are 16-byte aligned where they start
+    const bool dev = is_device_pointer(out) && (((uintptr_t)(out + done)) & 15) == 0;
+    if (done) e = cudaMemcpyAsync(out, q.buf + q.pos, done * sizeof(double), cudaMemcpyDefault, h->stream);
+    q.pos += done;
+    if (e != cudaSuccess) return cuda_err(e);
+    const uint64_t whole = (n - done) / epoch;
+    if (whole) {
+        if (dev) {
+            const int rc = seq_epochs(h, method, out + done, whole, mu, sigma);
+            if (rc != NRNG_OK) return rc;
+            done += whole * epoch;
+        } else {
+            for (uint64_t i = 0; i < whole; ++i, done += epoch) {
+                int rc = seq_epochs(h, method, q.buf, 1, mu, sigma);
+                if (rc != NRNG_OK) return rc;
+                e = cudaMemcpyAsync(out + done, q.buf, epoch * sizeof(double), cudaMemcpyDefault, h->stream);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+                if (e != cudaSuccess) return cuda_err(e);
+            }
+        }
+    }
+    if (done < n) {
+        const int rc = seq_epochs(h, method, q.buf, 1, mu, sigma);
+        if (rc != NRNG_OK) return rc;
+        q.len = epoch;
+        q.pos = n - done;
+        q.method = method;
+        q.mu = mu;
+        q.sigma = sigma;
+        e = cudaMemcpyAsync(out + done, q.buf, q.pos * sizeof(double), cudaMemcpyDefault, h->stream);
+        if (e != cudaSuccess) return cuda_err(e);
+    }
+    if (!dev) e = cudaStreamSynchronize(h->stream);
+    return cuda_err(e);
 }
 
 int nrng_uniform(nrng_handle h, double* out, size_t n) {

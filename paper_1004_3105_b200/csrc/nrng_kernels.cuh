@@ -20,7 +20,18 @@ struct BulkParams {
     uint32_t s_begin, s_end;
     TParams tp;
     int aligned;
+    // epoch layout (sequential mode, nrng_normal_seq): 0 = plain stream-major.  Otherwise
+    // every stream makes q = (#epochs) E pairs, E = 2^log2E, and pair j of stream k goes to
+    // pair slot (j / E) S E + k E + j mod E: the output is epoch-major, stream-major within
+    // an epoch, so consecutive calls continue one canonical sequence.
+    uint32_t log2E, S;
 };
+
+__device__ __forceinline__ uint64_t pair_slot(const BulkParams& p, uint64_t off, uint32_t k, uint64_t j) {
+    if (p.log2E == 0) return off + j;
+    const uint64_t E = 1ull << p.log2E;
+    return (j >> p.log2E) * ((uint64_t)p.S << p.log2E) + (uint64_t)k * E + (j & (E - 1));
+}
 
 // Per-block shared memory: [NW x kWinAlloc u64 windows][tables][per-kernel extras].
 // The bulk kernels come in two block shapes: NW = 4 warps (small stream counts: spread
@@ -127,6 +138,8 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
             double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
             const uint64_t full = qk.cnt - qk.cnt % (32 * kU);
             for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
+                if (p.log2E)  // epochs are multiples of 32 kU pairs: one slot computation per step
+                    o = reinterpret_cast<double2*>(p.out + (2 * pair_slot(p, qk.off, k, j0) - p.shift)) + lane;
                 lfg_ensure<kB>(L, lane, kNeedU);
                 double x[kU], y[kU];
                 bm_pairs<V, kU>(L.at(per * lane), p.tp, tab, x, y);
@@ -143,7 +156,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
             if ((uint32_t)lane < active) {
                 double x[1], y[1];
                 bm_pairs<V, 1>(L.at(per * lane), p.tp, tab, x, y);
-                store_pair(p.out, 2 * (qk.off + j0 + lane), p.shift, p.n, x[0], y[0], p.aligned);
+                store_pair(p.out, 2 * pair_slot(p, qk.off, k, j0 + lane), p.shift, p.n, x[0], y[0], p.aligned);
             }
             L.wc += per * active;
             __syncwarp();
@@ -238,7 +251,10 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 for (int u = 0; u < kPU; ++u) {
                     const uint32_t ju = j + __popc(m[u] & lt);
                     if ((m[u] >> lane) & 1u) {
-                        if (fast)
+                        if (p.log2E)
+                            __stcs(reinterpret_cast<double2*>(p.out + (2 * pair_slot(p, qk.off, k, base + ju) - p.shift)),
+                                   make_double2(ox[u], oy[u]));
+                        else if (fast)
                             __stcs(o + ju, make_double2(ox[u], oy[u]));
                         else
                             store_pair(p.out, 2 * (qk.off + base + ju), p.shift, p.n, ox[u], oy[u], p.aligned);

@@ -389,3 +389,45 @@ def test_statistical_gates_at_c3_size(method):
     assert abs(m2 - 1) < 4 * math.sqrt(2 / n)
     chi2 = np.sum((hist - n / K) ** 2 / (n / K))
     assert chi2 < sps.chi2.ppf(0.999, K - 1)
+
+
+# ---------------------------------------------------------------- sequential (RANN3-style) mode
+
+def _oracle_seq(seed, S, E, method, total, mu, sigma):
+    st = O.Streams(seed, S)
+    parts, got = [], 0
+    while got < total:
+        parts.append(ora_normals(st, method, 2 * S * E, mu, sigma))
+        got += 2 * S * E
+    return np.concatenate(parts)[:total]
+
+
+@pytest.mark.parametrize("method", ["B1", "B3", "P", "P2"])
+def test_sequential_mode_partition_invariant(method):
+    S, E = 256, 128
+    ep = 2 * S * E
+    total = 2 * ep + 12345
+    splits = [1, 6, ep - 3, ep + 1000, 0]
+    splits[-1] = total - sum(splits)
+    a, b = P.Generator(29, S), P.Generator(29, S)
+    one = host(a.normal_seq(method, total, 0.5, 2.0))
+    parts = [host(b.normal_seq(method, m, 0.5, 2.0)) for m in splits]
+    assert np.array_equal(one, np.concatenate(parts))  # any call partition: same sequence
+    o = _oracle_seq(29, S, E, method, total, 0.5, 2.0)
+    assert np.max(np.abs(one - o)) <= tol_for(method)
+    assert P.nrng_seq_buffered(a.h) == 3 * ep - total
+
+
+def test_sequential_mode_params_and_host_output():
+    S = 128
+    g = P.Generator(3, S)
+    g.normal_seq("B1", 1001)
+    with pytest.raises(P.NrngError):  # other method while B1 deviates are buffered
+        g.normal_seq("P", 10)
+    P.nrng_seq_reset(g.h)
+    g.normal_seq("P", 10)
+    a, b = P.Generator(4, S), P.Generator(4, S)
+    h = np.empty(3 * 2 * S * 128 + 77)
+    a.normal_seq("B2", out=h)
+    d = host(b.normal_seq("B2", h.size))
+    assert np.array_equal(h, d)
