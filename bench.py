@@ -255,6 +255,7 @@ def main():
         from statistics import NormalDist
 
         from paper_1004_3105_b200 import dist as D
+        from paper_1004_3105_b200 import gof as G
 
         K = 256
         edges = [CFG.mu + CFG.sigma * NormalDist().inv_cdf(i / K) for i in range(1, K)]
@@ -262,10 +263,16 @@ def main():
             g.normal(m, out=out, mu=CFG.mu, sigma=CFG.sigma)
             sums, hist = P.stats(out, CFG.mu, edges)
             sums, hist = D.allreduce_stats(sums, hist)  # NCCL: the run's only GPU<->GPU exchange
+            fine = P.gof_hist(out, CFG.mu, CFG.sigma, 20)
+            if world > 1:
+                dist.all_reduce(fine)
+            gofr = G.ks_ad(fine.cpu().numpy())
             sums, hist = sums.cpu().numpy(), hist.cpu().numpy()
             n = world * CFG.n
             v = D.moments(sums, n, CFG.sigma)
-            v.update({"chi2": D.chi_square(hist, n), "dof": K - 1, "min": float(sums[4]), "max": float(sums[5])})
+            v.update({"chi2": D.chi_square(hist, n), "dof": K - 1, "min": float(sums[4]), "max": float(sums[5]),
+                      "ks_d": gofr["ks_d"], "ks_pass": gofr["ks_pass"], "ad_a2": gofr["ad_a2"],
+                      "ad_pass": gofr["ad_pass"]})
             validation[m] = v
 
     # ---- e2e: the same step through the public API with HOST output buffers (pinned),

@@ -157,6 +157,14 @@ int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* de
 int nrng_stats(const double* dev_x, size_t n, double center, const double* dev_edges, int K, double* dev_sums,
                int64_t* dev_hist, void* cuda_stream);
 
+/* Goodness-of-fit histogram (gates as SPEC S:409-426): dev_hist[b]
+ * (2^log2K u32 counters, 4 <= log2K <= 24) counts x with Phi((x - mu)/sigma) in
+ * [b/K, (b+1)/K), K = 2^log2K.  The host computes the Kolmogorov-Smirnov and
+ * Anderson-Darling statistics from it (paper_1004_3105_b200/gof.py), after summing the
+ * histograms of all ranks.  Results are written, not accumulated.  sigma > 0. */
+int nrng_gof_hist(const double* dev_x, size_t n, double mu, double sigma, int log2K, uint32_t* dev_hist,
+                  void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,6 +50,7 @@ SIGNATURES = {
     "nrng_polar_mask": ([_p, _p, _sz], _int),
     "nrng_transform_from_uniforms": ([_p, _sz, _p, _p, _dbl, _dbl, _int, _p], _int),
     "nrng_stats": ([_p, _sz, _dbl, _p, _int, _p, _p, _p], _int),
+    "nrng_gof_hist": ([_p, _sz, _dbl, _dbl, _int, _p, _p], _int),
 }
 
 _lib = None
@@ -155,6 +156,10 @@ def nrng_transform_from_uniforms(u_ptr, n_pairs, out_ptr, mask_ptr, mu, sigma, m
 
 def nrng_stats(x_ptr, n, center, edges_ptr, K, sums_ptr, hist_ptr, stream) -> None:
     _check(lib().nrng_stats(x_ptr, n, center, edges_ptr, K, sums_ptr, hist_ptr, stream), "nrng_stats")
+
+
+def nrng_gof_hist(x_ptr, n, mu, sigma, log2K, hist_ptr, stream) -> None:
+    _check(lib().nrng_gof_hist(x_ptr, n, mu, sigma, log2K, hist_ptr, stream), "nrng_gof_hist")
 
 
 def nrng_last_error() -> int:
@@ -334,3 +339,11 @@ def stats(x, center: float, edges):
     nrng_stats(x.data_ptr(), x.numel(), center, edges.data_ptr(), K, sums.data_ptr(), hist.data_ptr(),
                _stream_ptr(torch))
     return sums, hist
+
+
+def gof_hist(x, mu: float, sigma: float, log2K: int = 20):
+    """Device histogram of Phi((x-mu)/sigma) over 2^log2K equal-probability bins (int32 tensor)."""
+    torch = _torch()
+    hist = torch.empty(1 << log2K, dtype=torch.int32, device=x.device)
+    nrng_gof_hist(x.data_ptr(), x.numel(), mu, sigma, log2K, hist.data_ptr(), _stream_ptr(torch))
+    return hist

@@ -499,6 +499,23 @@ int nrng_stats(const double* dev_x, size_t n, double center, const double* dev_e
     return cuda_err(e);
 }
 
+int nrng_gof_hist(const double* dev_x, size_t n, double mu, double sigma, int log2K, uint32_t* dev_hist,
+                  void* cuda_stream) {
+    if (log2K < 4 || log2K > 24 || !dev_hist || (n > 0 && !dev_x) || bad_params(mu, sigma) || !(sigma > 0))
+        return set_err(NRNG_EINVAL);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess) return set_err(NRNG_ENODEV);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    cudaError_t e = cudaMemsetAsync(dev_hist, 0, sizeof(uint32_t) << log2K, st);
+    if (e == cudaSuccess && n > 0) {
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * 16));
+        gof_hist_kernel<<<grid, 256, 0, st>>>(dev_x, n, mu, 1.0 / sigma, log2K, dev_hist);
+        e = cudaGetLastError();
+    }
+    return cuda_err(e);
+}
+
 int nrng_last_error(void) { return g_last; }
 
 const char* nrng_error_string(int code) {

@@ -508,4 +508,20 @@ __global__ void stats_final_kernel(const double* __restrict__ partial, int nbloc
     }
 }
 
+// ------------------------------------------------------------------ goodness of fit
+// Fine histogram of p = Phi((x - mu)/sigma) over K = 2^log2K equal-probability bins
+// (global u32 counters): the input of the KS and Anderson-Darling gates computed on the
+// host from the (all-reduced) histogram.  Validation only -- never in the timed region.
+__global__ void gof_hist_kernel(const double* __restrict__ x, uint64_t n, double mu, double inv_sigma, int log2K,
+                                unsigned int* __restrict__ hist) {
+    const double K = (double)(1u << log2K);
+    const unsigned kmax = (1u << log2K) - 1;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const double p = normcdf((x[i] - mu) * inv_sigma);
+        unsigned b = (unsigned)(p * K);
+        b = b > kmax ? kmax : b;
+        atomicAdd(&hist[b], 1u);
+    }
+}
+
 }  // namespace nrng

@@ -431,3 +431,28 @@ def test_sequential_mode_params_and_host_output():
     a.normal_seq("B2", out=h)
     d = host(b.normal_seq("B2", h.size))
     assert np.array_equal(h, d)
+
+
+# ---------------------------------------------------------------- goodness-of-fit histogram
+
+def test_gof_hist_matches_numpy():
+    from scipy import stats as sps
+
+    x = torch.from_numpy(W.dyadic_uniforms(90, 1 << 20) * 8 - 4).cuda()
+    for mu, sigma in ((0.0, 1.0), (0.3, 1.7)):
+        h = host(P.gof_hist(x, mu, sigma, 16)).astype(np.int64)
+        p = sps.norm.cdf((host(x) - mu) / sigma)
+        ref = np.bincount(np.minimum((p * (1 << 16)).astype(np.int64), (1 << 16) - 1), minlength=1 << 16)
+        assert h.sum() == x.numel()
+        assert np.sum(np.abs(h - ref)) <= 4  # Phi differs by ulps only at bin edges
+
+
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P", "P2"])
+def test_ks_ad_gates_at_c3_size(method):
+    from paper_1004_3105_b200 import gof
+
+    c = W.C3
+    g = P.Generator(c.seed + 7, c.streams)
+    x = g.normal(method, c.n, c.mu, c.sigma)
+    r = gof.ks_ad(host(P.gof_hist(x, c.mu, c.sigma, 20)))
+    assert r["n"] == c.n and r["ks_pass"] and r["ad_pass"], r
