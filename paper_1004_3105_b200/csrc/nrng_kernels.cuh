@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         lfg_load(L, rk, C, lane);
         const bool fast = p.aligned && 2 * (qk.off + qk.cnt) <= p.n;
+        const bool direct = fast && p.log2E == 0;
         for (uint64_t base = 0; base < qk.cnt;) {
             const uint32_t cnt = (uint32_t)(qk.cnt - base < (1ull << 31) ? qk.cnt - base : (1ull << 31));
             double2* o = reinterpret_cast<double2*>(p.out + (2 * (qk.off + base) - p.shift));
@@ -247,19 +248,26 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 else
                     polar_transform<kPU>(c, p.tp, tab, ox, oy);
                 uint32_t j = acc;
+                if (direct) {  // common case: one predicated 16-byte store per kept lane
 #pragma unroll
-                for (int u = 0; u < kPU; ++u) {
-                    const uint32_t ju = j + __popc(m[u] & lt);
-                    if ((m[u] >> lane) & 1u) {
-                        if (p.log2E)
-                            __stcs(reinterpret_cast<double2*>(p.out + (2 * pair_slot(p, qk.off, k, base + ju) - p.shift)),
-                                   make_double2(ox[u], oy[u]));
-                        else if (fast)
-                            __stcs(o + ju, make_double2(ox[u], oy[u]));
-                        else
-                            store_pair(p.out, 2 * (qk.off + base + ju), p.shift, p.n, ox[u], oy[u], p.aligned);
+                    for (int u = 0; u < kPU; ++u) {
+                        if ((m[u] >> lane) & 1u) __stcs(o + j + __popc(m[u] & lt), make_double2(ox[u], oy[u]));
+                        j += __popc(m[u]);
                     }
-                    j += __popc(m[u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kPU; ++u) {
+                        const uint32_t ju = j + __popc(m[u] & lt);
+                        if ((m[u] >> lane) & 1u) {
+                            if (p.log2E)
+                                __stcs(reinterpret_cast<double2*>(p.out +
+                                                                  (2 * pair_slot(p, qk.off, k, base + ju) - p.shift)),
+                                       make_double2(ox[u], oy[u]));
+                            else
+                                store_pair(p.out, 2 * (qk.off + base + ju), p.shift, p.n, ox[u], oy[u], p.aligned);
+                        }
+                        j += __popc(m[u]);
+                    }
                 }
                 acc = j;
                 L.wc += 2 * used;
