@@ -168,8 +168,7 @@ def emit_math(body):
     body.append("// max |r| = %.6e; ln(1+r) Taylor degree %d, truncation error %.3e" % (rmax, len(l1p) + 1, l1p_err))
     body.append("constexpr unsigned kLogBaseHi = 0x%08X;" % LOG_BASE_HI)
     body.append("constexpr int kLogTableBits = %d;" % LOG_TABLE_BITS)
-    body.append("constexpr double kLn2Hi = %s;" % rn(hi).hex())
-    body.append("constexpr double kLn2Lo = %s;" % rn(lo).hex())
+    body.append("constexpr double kLn2 = %s;" % rn(ln2).hex())
     body.append("// ln(1+r) = r + r^2 (L2 + r (L3 + ...))")
     body.append("__constant__ double kLog1p[%d] = {%s};" % (len(l1p), ", ".join(x.hex() for x in l1p)))
     body.append("// {inv_c_j, -ln(inv_c_j)} pairs")
