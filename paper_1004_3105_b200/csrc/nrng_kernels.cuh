@@ -282,30 +282,47 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
 }
 
 // ------------------------------------------------------------------ tiny quotas
-// Calls that give every stream only a few pairs (the C4 sweep: n <= 2^18 over 2^16
-// streams) are bound by per-stream latency and state traffic, not arithmetic: one THREAD
-// per stream generates its words straight through the HBM ring (x_{C+i} = ring[(C+i) mod
-// 607] + ring[(C+i+334) mod 607], written back in place -- exactly the recurrence, in the
-// canonical layout), transforms and stores.  Only the words actually used are touched.
+// Calls that give every stream only a few pairs (the C4 sweep: n <= 2^22 over 2^16 streams
+// gives 1-32 pairs per stream) are bound by per-stream latency and state traffic, not
+// arithmetic, and a warp would spend most of its time on one stream's state round trip.
+// Here one THREAD owns a stream and generates its words straight through the HBM ring in
+// the canonical layout: x_{C+i} = ring[(C+i) mod 607] + ring[(C+i+334) mod 607], written
+// back in place (exactly the recurrence), in chunks of 4 pairs whose 2 x 4 per source
+// words are loaded together (ILP) and transformed as one 4-wide batch.  Only the words
+// actually used are touched; unconsumed words of a Polar chunk are not written back.
 constexpr int kTinyThreads = 128;
-constexpr uint64_t kTinyMaxPairs = 4;  // per-stream quota routed here (8 words for B1)
+constexpr uint64_t kTinyMaxPairs = 32;  // per-stream quota routed here
 
-struct RingCursor {
-    uint64_t* r;
-    uint32_t a, b;  // positions of x_{n-607} (= slot of x_n) and x_{n-273}
-    __device__ __forceinline__ RingCursor(uint64_t* ring_k, uint64_t C) : r(ring_k) {
-        a = (uint32_t)(C % kLagR);
-        b = a + (kLagR - kLagS);
-        b = b >= (uint32_t)kLagR ? b - kLagR : b;
+// x_{n+t}, t < CW, where ring position a holds x_{n-607} (valid for CW <= 273).
+template <int CW>
+__device__ __forceinline__ void ring_peek(const uint64_t* __restrict__ r, uint32_t a, uint64_t (&w)[CW]) {
+    uint32_t b = a + (kLagR - kLagS);
+    b = b >= (uint32_t)kLagR ? b - kLagR : b;
+    uint64_t xa[CW], xb[CW];
+#pragma unroll
+    for (int t = 0; t < CW; ++t) {
+        uint32_t pa = a + t, pb = b + t;
+        pa = pa >= (uint32_t)kLagR ? pa - kLagR : pa;
+        pb = pb >= (uint32_t)kLagR ? pb - kLagR : pb;
+        xa[t] = r[pa];
+        xb[t] = r[pb];
     }
-    __device__ __forceinline__ uint64_t next() {
-        const uint64_t x = r[a] + r[b];
-        r[a] = x;
-        a = a + 1 == (uint32_t)kLagR ? 0 : a + 1;
-        b = b + 1 == (uint32_t)kLagR ? 0 : b + 1;
-        return x;
+#pragma unroll
+    for (int t = 0; t < CW; ++t) w[t] = xa[t] + xb[t];
+}
+// Write back the first `used` words (x_n at its own slot) and advance the cursor.
+template <int CW>
+__device__ __forceinline__ void ring_commit(uint64_t* __restrict__ r, uint32_t& a, const uint64_t (&w)[CW],
+                                            uint32_t used) {
+#pragma unroll
+    for (int t = 0; t < CW; ++t) {
+        uint32_t pa = a + t;
+        pa = pa >= (uint32_t)kLagR ? pa - kLagR : pa;
+        if ((uint32_t)t < used) r[pa] = w[t];
     }
-};
+    a += used;
+    a = a >= (uint32_t)kLagR ? a - kLagR : a;
+}
 
 template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2
 __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
@@ -317,35 +334,68 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
     const Quota qk = quota(p.q, p.rem, k);
     if (qk.cnt == 0) return;
     const uint64_t C = p.count[k];
-    RingCursor rc(p.ring + (uint64_t)k * kPitch, C);
+    uint64_t* r = p.ring + (uint64_t)k * kPitch;
+    uint32_t a = (uint32_t)(C % kLagR);
     uint64_t used = 0;
-    for (uint64_t j = 0; j < qk.cnt; ++j) {
-        double x[1], y[1];
+    constexpr int per = (V == 3) ? 3 : 2;
+    constexpr int CW = 4 * per;
+    uint32_t j = 0;  // pairs done
+    while (j < qk.cnt) {
+        uint64_t w[CW];
+        ring_peek<CW>(r, a, w);
+        double x[4], y[4];
+        uint32_t take, words;
         if (V >= 4) {
-            PolarCand c[1];
-            bool ok;
-            do {
-                const uint64_t wa = rc.next(), wb = rc.next();
-                used += 2;
-                ok = polar_candidate(wa, wb, c[0]);
-            } while (!ok);
+            PolarCand c[4];
+            bool ok[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) ok[t] = polar_candidate(w[2 * t], w[2 * t + 1], c[t]);
             if (V == 5)
-                p2_transform<1>(c, p.tp, tab, x, y);
+                p2_transform<4>(c, p.tp, tab, x, y);
             else
-                polar_transform<1>(c, p.tp, tab, x, y);
-        } else if (V == 3) {
-            const uint64_t w1[1] = {rc.next()}, w2[1] = {rc.next()}, w3[1] = {rc.next()};
-            used += 3;
-            b3_pairs<1>(w1, w2, w3, p.tp, tab, x, y);
+                polar_transform<4>(c, p.tp, tab, x, y);
+            uint32_t got = 0, cand = 4;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (ok[t] && j + got < qk.cnt) {
+                    store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + got), p.shift, p.n, x[t], y[t], p.aligned);
+                    if (j + ++got == qk.cnt) cand = t + 1;  // exact stop: nothing after the last accept
+                }
+            }
+            take = got;
+            words = 2 * cand;
         } else {
-            const uint64_t wu[1] = {rc.next()}, wv[1] = {rc.next()};
-            used += 2;
-            if (V == 1)
-                b1_pairs<1>(wu, wv, p.tp, tab, x, y);
-            else
-                b2_pairs<1>(wu, wv, p.tp, tab, x, y);
+            if (V == 3) {
+                uint64_t w1[4], w2[4], w3[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    w1[t] = w[3 * t];
+                    w2[t] = w[3 * t + 1];
+                    w3[t] = w[3 * t + 2];
+                }
+                b3_pairs<4>(w1, w2, w3, p.tp, tab, x, y);
+            } else {
+                uint64_t wu[4], wv[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    wu[t] = w[2 * t];
+                    wv[t] = w[2 * t + 1];
+                }
+                if (V == 1)
+                    b1_pairs<4>(wu, wv, p.tp, tab, x, y);
+                else
+                    b2_pairs<4>(wu, wv, p.tp, tab, x, y);
+            }
+            take = qk.cnt - j < 4 ? (uint32_t)(qk.cnt - j) : 4u;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if ((uint32_t)t < take)
+                    store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + t), p.shift, p.n, x[t], y[t], p.aligned);
+            words = per * take;
         }
-        store_pair(p.out, 2 * (qk.off + j), p.shift, p.n, x[0], y[0], p.aligned);
+        ring_commit<CW>(r, a, w, words);
+        used += words;
+        j += take;
     }
     p.count[k] = C + used;
 }
