@@ -38,7 +38,10 @@ __device__ __forceinline__ uint64_t pair_slot(const BulkParams& p, uint64_t off,
 // over all SMs) and NW = kBigBlock warps, one block per SM (the tables are stored once per
 // SM instead of once per 4 warps, which is what lets 20 windows fit in 227 KB).
 constexpr size_t win_bytes(int nw) { return (size_t)nw * kWinAlloc * sizeof(uint64_t); }
-constexpr int kBigBlock = 20;
+#ifndef NRNG_BIGBLOCK
+#define NRNG_BIGBLOCK 20
+#endif
+constexpr int kBigBlock = NRNG_BIGBLOCK;
 constexpr int kBigBlockPolar = 20;
 
 // ------------------------------------------------------------------ seeding + warm-up
@@ -118,7 +121,10 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr uint32_t per = (V == 3) ? 3 : 2;
-    constexpr int kU = (V == 3) ? 2 : 4;               // pairs per lane per main-loop iteration
+#ifndef NRNG_B3_U
+#define NRNG_B3_U 2
+#endif
+    constexpr int kU = (V == 3) ? NRNG_B3_U : 4;       // pairs per lane per main-loop iteration
     constexpr int kB = 128;                            // refill batch
     constexpr uint32_t kNeedU = 32 * kU * per;         // words per main-loop iteration
     static_assert(kNeedU - 1 + kB <= kWin - kLagR, "lookahead would clobber the write-back words");
