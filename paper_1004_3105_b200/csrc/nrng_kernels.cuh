@@ -143,6 +143,27 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
         if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
             double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
             const uint64_t full = qk.cnt - qk.cnt % (32 * kU);
+            if (kNeedU == kBlk && full > 0) {  // B1/B2: phased steady state (one block per iteration)
+                lfg_generate<kBlk>(L, lane);    // block 0
+                uint64_t* bl = L.buf + lane;
+                uint32_t ph = 0;
+                for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
+                    if (p.log2E)
+                        o = reinterpret_cast<double2*>(p.out + (2 * pair_slot(p, qk.off, k, j0) - p.shift)) + lane;
+                    const uint32_t nb = (ph + 1) & 3;
+                    uint64_t g[kBlkW];
+                    phase_gen_load(bl, nb, g);
+                    double x[kU], y[kU];
+                    bm_pairs<V, kU>(L.buf + kBlk * ph + per * lane, p.tp, tab, x, y);
+                    phase_gen_store(bl, nb, g);
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+                    __syncwarp();
+                    ph = nb;
+                }
+                L.wc = kW0 + (uint32_t)(per * full);
+                L.wg = L.wc + kBlk;
+            }
             for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
                 if (p.log2E)  // epochs are multiples of 32 kU pairs: one slot computation per step
                     o = reinterpret_cast<double2*>(p.out + (2 * pair_slot(p, qk.off, k, j0) - p.shift)) + lane;
@@ -192,6 +213,41 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
 constexpr int kPU = NRNG_POLAR_U;  // candidates per lane per step (32 kPU per warp)
 constexpr int kPB = 128; // refill batch: lookahead 64 kPU - 1 + kPB <= 417
 static_assert(64 * kPU - 1 + kPB <= kWin - kLagR && 64 * kPU <= kMirror, "polar window bounds");
+
+// Rank the accepts of one step (candidate i = 32 u + lane) and, if the step reaches the
+// remaining quota `need`, keep only the first `need` of them (exact stop, R5).  m[u] =
+// kept accept masks; returns the candidates consumed (32 kPU unless the step stops).
+__device__ __forceinline__ uint32_t polar_rank(const bool (&ok)[kPU], unsigned (&m)[kPU], uint32_t need, unsigned lt,
+                                               bool& stop) {
+    uint32_t tot = 0;
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) {
+        m[u] = __ballot_sync(kFull, ok[u]);
+        tot += __popc(m[u]);
+    }
+    uint32_t used = 32 * kPU;
+    stop = tot >= need;
+    if (stop) {
+        uint32_t rem = need;
+#pragma unroll
+        for (int u = 0; u < kPU; ++u) {
+            const uint32_t nu = __popc(m[u]);
+            if (rem == 0) {
+                m[u] = 0;
+            } else if (nu >= rem) {
+                const unsigned last = __ballot_sync(kFull, ok[u] && (uint32_t)__popc(m[u] & lt) == rem - 1);
+                const int l = __ffs(last) - 1;
+                m[u] &= (l == 31) ? kFull : ((2u << l) - 1u);
+                used = 32 * u + l + 1;
+                rem = 0;
+            } else {
+                rem -= nu;
+            }
+        }
+    }
+    return used;
+}
+
 template <int NW, int M>
 __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
@@ -209,7 +265,53 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
         lfg_load(L, rk, C, lane);
         const bool fast = p.aligned && 2 * (qk.off + qk.cnt) <= p.n;
         const bool direct = fast && p.log2E == 0;
-        for (uint64_t base = 0; base < qk.cnt;) {
+        const bool phased = direct && qk.cnt < (1ull << 31);
+        if (phased) {
+            // Phased steady state: every step but the stream's last consumes exactly one
+            // 256-word block (128 candidates) and generates the next; the last step (exact
+            // stop) generates nothing, so the lookahead stays <= 256 for the write-back.
+            static_assert(64 * kPU == kBlk, "one block per polar step");
+            lfg_generate<kBlk>(L, lane);  // block 0
+            uint64_t* bl = L.buf + lane;
+            double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift));
+            const uint32_t cnt = (uint32_t)qk.cnt;
+            uint32_t ph = 0, acc = 0, it = 0;
+            for (;;) {
+                const uint32_t nb = (ph + 1) & 3;
+                uint64_t g[kBlkW];
+                phase_gen_load(bl, nb, g);
+                PolarCand c[kPU];
+                bool ok[kPU];
+                unsigned m[kPU];
+#pragma unroll
+                for (int u = 0; u < kPU; ++u) {
+                    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(L.buf + kBlk * ph + 64 * u + 2 * lane);
+                    ok[u] = polar_candidate(w.x, w.y, c[u]);
+                }
+                bool stop;
+                const uint32_t used = polar_rank(ok, m, cnt - acc, lt, stop);
+                if (!stop) phase_gen_store(bl, nb, g);
+                double ox[kPU], oy[kPU];
+                if (M == 2)
+                    p2_transform<kPU>(c, p.tp, tab, ox, oy);
+                else
+                    polar_transform<kPU>(c, p.tp, tab, ox, oy);
+#pragma unroll
+                for (int u = 0; u < kPU; ++u) {
+                    if ((m[u] >> lane) & 1u) __stcs(o + acc + __popc(m[u] & lt), make_double2(ox[u], oy[u]));
+                    acc += __popc(m[u]);
+                }
+                __syncwarp();
+                if (stop) {
+                    L.wc = kW0 + kBlk * it + 2 * used;
+                    L.wg = kW0 + kBlk * (it + 1);
+                    break;
+                }
+                ++it;
+                ph = nb;
+            }
+        }
+        for (uint64_t base = 0; !phased && base < qk.cnt;) {  // general path
             const uint32_t cnt = (uint32_t)(qk.cnt - base < (1ull << 31) ? qk.cnt - base : (1ull << 31));
             double2* o = reinterpret_cast<double2*>(p.out + (2 * (qk.off + base) - p.shift));
             uint32_t acc = 0;  // accepted pairs of this chunk
@@ -223,31 +325,8 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                     const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(L.at(64 * u + 2 * lane));
                     ok[u] = polar_candidate(w.x, w.y, c[u]);
                 }
-                uint32_t tot = 0;
-#pragma unroll
-                for (int u = 0; u < kPU; ++u) {
-                    m[u] = __ballot_sync(kFull, ok[u]);
-                    tot += __popc(m[u]);
-                }
-                uint32_t used = 32 * kPU;
-                if (tot >= cnt - acc) {  // exact stop: keep the first `need` accepts in candidate order
-                    uint32_t rem = cnt - acc;
-#pragma unroll
-                    for (int u = 0; u < kPU; ++u) {
-                        const uint32_t nu = __popc(m[u]);
-                        if (rem == 0) {
-                            m[u] = 0;
-                        } else if (nu >= rem) {
-                            const unsigned last = __ballot_sync(kFull, ok[u] && (uint32_t)__popc(m[u] & lt) == rem - 1);
-                            const int l = __ffs(last) - 1;
-                            m[u] &= (l == 31) ? kFull : ((2u << l) - 1u);
-                            used = 32 * u + l + 1;
-                            rem = 0;
-                        } else {
-                            rem -= nu;
-                        }
-                    }
-                }
+                bool stop;
+                const uint32_t used = polar_rank(ok, m, cnt - acc, lt, stop);
                 double ox[kPU], oy[kPU];
                 if (M == 2)
                     p2_transform<kPU>(c, p.tp, tab, ox, oy);

@@ -87,7 +87,7 @@ def generate():
 # error (< 1e-16 absolute on the reduced arguments) sits far inside the 1e-13 output bar.
 
 LOG_BASE_HI = 0x3FE6A09E  # high word of sqrt(1/2): m is normalised into [sqrt(1/2), sqrt(2))
-LOG_TABLE_BITS = 8
+LOG_TABLE_BITS = 7  # 128 buckets: the table is stored 8x interleaved (bank-conflict-free, 16 KB)
 
 
 def _d_from_hi(hi):
@@ -112,10 +112,18 @@ def log_table():
 
 
 def log1p_coeffs(rmax, degree=5):
-    """Taylor coefficients of ln(1+r) = r + sum_{k=2..degree} (-1)^(k+1) r^k / k; truncation
-    error rmax^(degree+1)/(degree+1)."""
-    err = rmax ** (degree + 1) / (degree + 1)
-    return [rn(mp.mpf((-1) ** (k + 1)) / k) for k in range(2, degree + 1)], err
+    """ln(1+r) = r + r^2 P(r) on |r| <= rmax, P of degree `degree` - 2: the Chebyshev
+    interpolant of (ln(1+r) - r)/r^2 (r = 0: -1/2), so the r and r^2 terms stay exact-leading
+    and the relative accuracy as r -> 0 is kept.  Returns (coefficients of P, max error of
+    r + r^2 P(r) on a fine grid, in exact arithmetic)."""
+    a = mp.mpf(rmax)
+    f = lambda r: (mp.log1p(r) - r) / (r * r) if r != 0 else mp.mpf(-1) / 2
+    P = [rn(x) for x in _cheb_fit_interval(f, -a, a, degree - 2)]
+    err = mp.mpf(0)
+    for i in range(-400, 401):
+        r = a * i / 400
+        err = max(err, abs(r + r * r * mp.fsum(c * r ** k for k, c in enumerate(P)) - mp.log1p(r)))
+    return P, float(err)
 
 
 def _cheb_fit_interval(f, a, b, degree):
@@ -165,7 +173,7 @@ def emit_math(body):
     lo = ln2 - hi
     body.append("// ---- path primitives (implementation constants, DESIGN.md §6) ----")
     body.append("// ln: m in [sqrt(1/2), sqrt(2)), bucket j = top %d bits of m's 20-bit high mantissa field;" % LOG_TABLE_BITS)
-    body.append("// max |r| = %.6e; ln(1+r) Taylor degree %d, truncation error %.3e" % (rmax, len(l1p) + 1, l1p_err))
+    body.append("// max |r| = %.6e; ln(1+r) = r + r^2 P(r), P Chebyshev degree %d, max error %.3e" % (rmax, len(l1p) - 1, l1p_err))
     body.append("constexpr unsigned kLogBaseHi = 0x%08X;" % LOG_BASE_HI)
     body.append("constexpr int kLogTableBits = %d;" % LOG_TABLE_BITS)
     body.append("constexpr double kLn2 = %s;" % rn(ln2).hex())
