@@ -143,8 +143,10 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
         if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
             double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
             const uint64_t full = qk.cnt - qk.cnt % (32 * kU);
-            if (kNeedU == kBlk && full > 0) {  // B1/B2: phased steady state (one block per iteration)
-                lfg_generate<kBlk>(L, lane);    // block 0
+            if constexpr (V == 2) if (full > 0) {
+                // B2 phased steady state: iteration b transforms block b from the window and
+                // generates block b + 1 word-wise (measured faster than pair rows for B2).
+                lfg_generate<kBlk>(L, lane);  // block 0
                 uint64_t* bl = L.buf + lane;
                 uint32_t ph = 0;
                 for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
@@ -163,6 +165,49 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
                 }
                 L.wc = kW0 + (uint32_t)(per * full);
                 L.wg = L.wc + kBlk;
+            }
+            if constexpr (V == 1) if (full > 0) {
+                // B1 phased steady state: iteration b generates block b (positions 256 (b
+                // mod 4) ..) as four pair rows and transforms it from registers.
+                static_assert(kU == 4 && kNeedU == kBlk, "one pair row per transform slot");
+                uint64_t carry = block_first_word(L.buf, 0);
+                uint32_t ph = 0;
+                for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
+                    if (p.log2E)
+                        o = reinterpret_cast<double2*>(p.out + (2 * pair_slot(p, qk.off, k, j0) - p.shift)) + lane;
+                    uint64_t wu[kU], wv[kU];
+#ifndef NRNG_EXP_NOLFG
+                    const PairRowPtrs r = pair_row_ptrs(L.buf, ph, lane);
+                    gen_pair_rows<kU>(r.sa, r.sb, r.d, ph == 0, lane, carry, wu, wv);
+#else  // experiment: transform cost alone (words from a counter, no window traffic)
+#pragma unroll
+                    for (int t = 0; t < kU; ++t) { wu[t] = (j0 + t) * 0x9E3779B97F4A7C15ull + lane; wv[t] = wu[t] * 0xBF58476D1CE4E5B9ull; }
+#endif
+                    double x[kU], y[kU];
+#ifndef NRNG_EXP_NOTRANSFORM
+                    if (V == 1)
+                        b1_pairs<kU>(wu, wv, p.tp, tab, x, y);
+                    else
+                        b2_pairs<kU>(wu, wv, p.tp, tab, x, y);
+#else  // experiment: generator + stores alone
+#pragma unroll
+                    for (int t = 0; t < kU; ++t) { x[t] = __longlong_as_double(wu[t] >> 2); y[t] = __longlong_as_double(wv[t] >> 2); }
+#endif
+#if defined(NRNG_EXP_PLAINSTORE)
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) o[32 * u] = make_double2(x[u], y[u]);
+#elif !defined(NRNG_EXP_NOSTORE)
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+#else  // experiment: no output traffic (a never-taken store keeps the transform alive)
+#pragma unroll
+                    for (int u = 0; u < kU; ++u)
+                        if (x[u] == 1234.5 && y[u] == 1234.5) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+#endif
+                    __syncwarp();
+                    ph = (ph + 1) & 3;
+                }
+                L.wc = L.wg = kW0 + (uint32_t)(per * full);
             }
             for (; j0 < full; j0 += 32 * kU, o += 32 * kU) {
                 if (p.log2E)  // epochs are multiples of 32 kU pairs: one slot computation per step
