@@ -100,7 +100,9 @@ enum class Kind { BM1, BM2, BM3, POLAR, POLAR2, UNIFORM };
 
 template <int V>
 void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
-    if (ns >= (uint32_t)(kBigBlock * h->num_sms))
+    if (V == 3 && p.aligned && p.log2E == 0 && ns >= (uint32_t)(kTriWarps * h->num_sms))
+        b3_kernel<kTriWarps><<<h->num_sms, kTriWarps * 32, tri_smem(kTriWarps), st>>>(p);
+    else if (ns >= (uint32_t)(kBigBlock * h->num_sms))
         bm_kernel<V, kBigBlock><<<h->num_sms, kBigBlock * 32, bm_smem(kBigBlock), st>>>(p);
     else
         bm_kernel<V, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.bm[V], h->num_sms), kWarpsPerBlock * 32,
@@ -178,7 +180,7 @@ int run_bulk(nrng_handle h, Kind kind, double* out, size_t n, uint64_t units, in
     p.q = units / h->S;
     p.rem = units % h->S;
     p.n = n;
-    p.tp = TParams{mu, sigma, 2.0 * sigma};
+    p.tp = TParams{mu, sigma, sigma * 0x1.6a09e667f3bcdp+0};
     const uint32_t active = p.q == 0 ? (uint32_t)p.rem : h->S;  // streams with work
     if (is_device_pointer(out)) {
         p.out = out;
@@ -255,6 +257,7 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(bm_kernel<1, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(bm_kernel<2, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(bm_kernel<3, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
+    occupancy(b3_kernel<kTriWarps>, kTriWarps, tri_smem(kTriWarps));
     occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     occupancy(polar_kernel<kBigBlockPolar, 2>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     h->occ.uni = occupancy(uniform_kernel, kWarpsPerBlock, kUniSmem);
@@ -359,7 +362,7 @@ int seq_epochs(nrng_handle h, int method, double* dst, uint64_t epochs, double m
     p.rem = 0;
     p.units = p.q * h->S;
     p.n = 2 * p.units;
-    p.tp = TParams{mu, sigma, 2.0 * sigma};
+    p.tp = TParams{mu, sigma, sigma * 0x1.6a09e667f3bcdp+0};
     p.out = dst;
     p.shift = 0;
     p.aligned = ((uintptr_t)dst & 15) == 0;
@@ -472,7 +475,7 @@ int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* de
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)std::min<uint64_t>((n_pairs + 255) / 256, (uint64_t)sms * 8);
     transform_kernel<<<grid, 256, 0, (cudaStream_t)cuda_stream>>>(dev_u, n_pairs, dev_out, dev_mask,
-                                                                  TParams{mu, sigma, 2.0 * sigma}, method);
+                                                                  TParams{mu, sigma, sigma * 0x1.6a09e667f3bcdp+0}, method);
     return cuda_err(cudaGetLastError());
 }
 

@@ -239,6 +239,142 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
     }
 }
 
+// ------------------------------------------------------------------ B3, triple rows
+// B3 consumes the stream in word triples (u1, u2, u3).  Here each lane
+// GENERATES the three consecutive words it consumes: lane l makes x_{R+3l+i}, i < 3, of
+// the 96-word row starting at R from x_{R+3l+i-607} and x_{R+3l+i-273} (rows are shorter
+// than the 273 lag, so every source is older than the row), stores them and transforms
+// them from registers.  A 64-bit access at a 3-word lane stride is bank-conflict-free (the
+// 16 lanes of a half-warp hit bank pairs 6l mod 32, all distinct), so a row costs 6 loads
+// and 3 stores of 256 B each: 24 B of shared traffic per word, against 34 B for a
+// word-wise refill plus the consumer's re-read.  The window is 9 rows (864 words >= 607
+// + the 2 rows of an iteration) plus a 2-row mirror of rows 0-1 for the sources that run
+// past its end (8.25 KB per warp, 24 warps per SM).  Word i of the call (i < 0: the
+// loaded state) sits at window position i mod 864.
+constexpr int kTriRow = 96;
+constexpr int kTriWin = 9 * kTriRow;
+constexpr int kTriMirror = 2 * kTriRow;
+constexpr int kTriAlloc = kTriWin + kTriMirror;
+constexpr int kTriScratch = 32;  // per-warp tail-compaction slots (doubles)
+constexpr int kTriWarps = 24;
+static_assert(kTriWin >= kLagR + 2 * kTriRow && kTriRow < kLagS, "triple-row window");
+constexpr size_t tri_smem(int nw) {
+    return (size_t)nw * (kTriAlloc + kTriScratch) * sizeof(uint64_t) + kTabBytes;
+}
+
+__device__ __forceinline__ uint32_t tri_wrap(uint32_t x) { return x >= (uint32_t)kTriWin ? x - kTriWin : x; }
+
+// Window positions of an iteration's first row and of its two source runs.
+struct TriPos {
+    uint32_t d, a, b;  // row 0 at d; sources x_{w-607} at a, x_{w-273} at b (row t at +96 t, via the mirror)
+    __device__ __forceinline__ void advance(uint32_t rows) {
+        d = tri_wrap(d + kTriRow * rows);
+        a = tri_wrap(a + kTriRow * rows);
+        b = tri_wrap(b + kTriRow * rows);
+    }
+};
+
+// Generate R (<= 2) consecutive rows at `ps`.  All loads are issued before any store (the
+// rows' sources are all older than the rows).
+template <int R>
+__device__ __forceinline__ void gen_tri_rows(uint64_t* buf, const TriPos& ps, int lane, uint64_t (&w1)[R],
+                                             uint64_t (&w2)[R], uint64_t (&w3)[R]) {
+    static_assert(R <= 2, "mirror covers two rows of source overrun");
+    uint64_t a[R][3], b[R][3];
+    const uint64_t* sa = buf + ps.a + 3 * lane;
+    const uint64_t* sb = buf + ps.b + 3 * lane;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            a[t][i] = sa[kTriRow * t + i];
+            b[t][i] = sb[kTriRow * t + i];
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        w1[t] = a[t][0] + b[t][0];
+        w2[t] = a[t][1] + b[t][1];
+        w3[t] = a[t][2] + b[t][2];
+        const uint32_t pd = t == 0 ? ps.d : tri_wrap(ps.d + kTriRow * t);
+        uint64_t* d = buf + pd + 3 * lane;
+        d[0] = w1[t];
+        d[1] = w2[t];
+        d[2] = w3[t];
+        if (pd < (uint32_t)kTriMirror) {  // rows 0-1 are mirrored past the end
+            d[kTriWin] = w1[t];
+            d[kTriWin + 1] = w2[t];
+            d[kTriWin + 2] = w3[t];
+        }
+    }
+}
+
+// Aligned, plain-layout B3 calls (the dispatcher sends the rest to bm_kernel<3>).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
+    extern __shared__ __align__(16) uint64_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * (kTriAlloc + kTriScratch)));
+    __syncthreads();
+    uint64_t* const buf = smem + warp * (kTriAlloc + kTriScratch);
+    double* const scr = reinterpret_cast<double*>(buf + kTriAlloc);
+    const unsigned lt = lanemask_lt(lane);
+    for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
+        const Quota qk = quota(p.q, p.rem, k);
+        if (qk.cnt == 0) continue;
+        const uint64_t C = p.count[k];
+        uint64_t* rk = p.ring + (uint64_t)k * kPitch;
+        {   // x_{C-607+j} -> position 864 - 607 + j
+            const uint32_t base = (uint32_t)(C % kLagR);
+            for (int j = lane; j < kLagR; j += 32) {
+                uint32_t q = base + j;
+                q = q >= (uint32_t)kLagR ? q - kLagR : q;
+                buf[(kTriWin - kLagR) + j] = rk[q];
+            }
+        }
+        __syncwarp();
+        // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
+        const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
+        const uint64_t full2 = safe_cnt - safe_cnt % 64;
+        double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
+        TriPos ps{0, kTriWin - kLagR, kTriWin - kLagS};
+        uint64_t j0 = 0;
+        for (; j0 < full2; j0 += 64, o += 64) {
+            uint64_t w1[2], w2[2], w3[2];
+            gen_tri_rows<2>(buf, ps, lane, w1, w2, w3);
+            double x[2], y[2];
+            b3_pairs_compact<2>(w1, w2, w3, p.tp, tab, scr, lane, lt, x, y);
+            __stcs(o, make_double2(x[0], y[0]));
+            __stcs(o + 32, make_double2(x[1], y[1]));
+            __syncwarp();
+            ps.advance(2);
+        }
+        for (; j0 < qk.cnt; j0 += 32) {  // the last rows, possibly partial, and the unsafe pair
+            uint64_t w1[1], w2[1], w3[1];
+            gen_tri_rows<1>(buf, ps, lane, w1, w2, w3);
+            double x[1], y[1];
+            b3_pairs<1>(w1, w2, w3, p.tp, tab, x, y);
+            if ((uint64_t)lane < qk.cnt - j0)
+                store_pair(p.out, 2 * (qk.off + j0 + lane), p.shift, p.n, x[0], y[0], true);
+            __syncwarp();
+            ps.advance(1);
+        }
+        // write back the last min(3 cnt, 607) consumed words (relative index i at i mod 864)
+        const uint64_t used = 3 * qk.cnt;
+        const uint32_t nw = used < (uint64_t)kLagR ? (uint32_t)used : (uint32_t)kLagR;
+        const uint32_t pos0 = (uint32_t)((used - nw) % kTriWin);  // used - nw >= 0
+        const uint32_t slot0 = (uint32_t)((C + used - nw) % kLagR);
+        for (uint32_t j = lane; j < nw; j += 32) {
+            uint32_t pp = pos0 + j, q = slot0 + j;
+            pp = pp >= (uint32_t)kTriWin ? pp - kTriWin : pp;
+            q = q >= (uint32_t)kLagR ? q - kLagR : q;
+            rk[q] = buf[pp];
+        }
+        if (lane == 0) p.count[k] = C + used;
+        __syncwarp();
+    }
+}
+
 // ------------------------------------------------------------------ Polar P
 // 64 candidates (128 uniforms) per warp step, two per lane: candidate i of the step is
 // lane i%32's (i < 32: words wc + 2i, i >= 32: wc + 64 + 2(i-32)).  Accepts are ranked

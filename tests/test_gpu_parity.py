@@ -254,6 +254,20 @@ def test_small_and_odd_n(n, method):
     assert_state_equal(g, st)
 
 
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P", "P2"])
+def test_wide_ragged_calls(method):
+    # >= 28 x 148 streams: the one-block-per-SM kernels (B3's triple-row kernel included)
+    # with ragged per-stream quotas (remainder streams, a partial last row, a dropped odd
+    # deviate) over consecutive calls, every stream against the oracle, state bit-exact.
+    S = 4160
+    g, st = P.Generator(12, S, first_stream=77), O.Streams(12, S, first_stream=77)
+    for n in (2 * S * 70 + 2 * 1234 + 1, 2 * S * 37 + 2 * 4000, 2 * S * 64 + 2 * 17 + 1):
+        d = gen_normals(g, method, n, -0.25, 1.5)
+        o = ora_normals(st, method, n, -0.25, 1.5)
+        assert d.size == n and np.max(np.abs(d - o)) <= tol_for(method), (method, n)
+    assert_state_equal(g, st)
+
+
 def test_invalid_arguments():
     g = P.Generator(1, 8)
     out = torch.empty(16, dtype=torch.float64, device="cuda")
