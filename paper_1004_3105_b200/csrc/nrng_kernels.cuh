@@ -143,7 +143,10 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
         if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
             double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
             const uint64_t full = qk.cnt - qk.cnt % (32 * kU);
-            if constexpr (V == 2) if (full > 0) {
+            // B1: pair rows; B2: word-wise (measured faster for B2, whose sincos16 has no
+            // integer work to hide the generator's latencies behind)
+            constexpr bool kPairRows = V == 1;
+            if constexpr (V == 2 && !kPairRows) if (full > 0) {
                 // B2 phased steady state: iteration b transforms block b from the window and
                 // generates block b + 1 word-wise (measured faster than pair rows for B2).
                 lfg_generate<kBlk>(L, lane);  // block 0
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
                 L.wc = kW0 + (uint32_t)(per * full);
                 L.wg = L.wc + kBlk;
             }
-            if constexpr (V == 1) if (full > 0) {
+            if constexpr (kPairRows) if (full > 0) {
                 // B1 phased steady state: iteration b generates block b (positions 256 (b
                 // mod 4) ..) as four pair rows and transforms it from registers.
                 static_assert(kU == 4 && kNeedU == kBlk, "one pair row per transform slot");
@@ -452,18 +455,18 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
             // 256-word block (128 candidates) and generates the next; the last step (exact
             // stop) generates nothing, so the lookahead stays <= 256 for the write-back.
             static_assert(64 * kPU == kBlk, "one block per polar step");
-            lfg_generate<kBlk>(L, lane);  // block 0
-            uint64_t* bl = L.buf + lane;
             double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift));
             const uint32_t cnt = (uint32_t)qk.cnt;
             uint32_t ph = 0, acc = 0, it = 0;
+            lfg_generate<kBlk>(L, lane);  // block 0
+            uint64_t* bl = L.buf + lane;
             for (;;) {
-                const uint32_t nb = (ph + 1) & 3;
-                uint64_t g[kBlkW];
-                phase_gen_load(bl, nb, g);
                 PolarCand c[kPU];
                 bool ok[kPU];
                 unsigned m[kPU];
+                const uint32_t nb = (ph + 1) & 3;
+                uint64_t g[kBlkW];
+                phase_gen_load(bl, nb, g);
 #pragma unroll
                 for (int u = 0; u < kPU; ++u) {
                     const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(L.buf + kBlk * ph + 64 * u + 2 * lane);
@@ -479,7 +482,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                     polar_transform<kPU>(c, p.tp, tab, ox, oy);
 #pragma unroll
                 for (int u = 0; u < kPU; ++u) {
-                    if ((m[u] >> lane) & 1u) __stcs(o + acc + __popc(m[u] & lt), make_double2(ox[u], oy[u]));
+                    if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), make_double2(ox[u], oy[u]));
                     acc += __popc(m[u]);
                 }
                 __syncwarp();
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                     break;
                 }
                 ++it;
-                ph = nb;
+                ph = (ph + 1) & 3;
             }
         }
         for (uint64_t base = 0; !phased && base < qk.cnt;) {  // general path
