@@ -34,14 +34,16 @@ METHODS = ("B1", "B2", "B3", "P")
 CFG = W.C5_SHARD
 BYTES_PER_NORMAL = 8  # algorithmic HBM traffic: one fp64 written per normal
 # Algorithmic FP64 work per pair ("roofline"): the paper's operation sequence
-# for each method, priced with the DP-pipe cost of double-accurate primitives
-# (ln 9, radius sigma sqrt(-2 ln) 10, sin+cos of an exactly reduced angle 14, IEEE divide 7,
-# sincos16 of P:162-170 21, Horner-15 15; MUFU seeds and integer work not counted):
-#   B1 = ln + radius + sincos + 2 outputs                     = 35
-#   B2 = ln + radius + sincos16 + 2                           = 42
-#   B3 = bulk (u, 2 fma, div, Horner, 3 mul, sincos16, 2) 51, tail (1/9) 7 fewer  = 50.2
-#   P  = (4/pi) candidates x 3 + ln + 1 + 1 + Newton 6 + 2 + 2 = 24.8
-DP_PER_PAIR = {"B1": 35.0, "B2": 42.0, "B3": 51.0 - 7.0 / 9.0, "P": 3.0 * 4.0 / math.pi + 21.0}
+# for each method, priced with the DP-pipe cost of the cheapest double-accurate primitives
+# we have (table ln 8, radius from ln by one third-order rsqrt step 7, sin+cos of an exactly
+# reduced angle 14, IEEE divide 8, sincos16 of P:162-170 21, Horner-15 15; MUFU seeds and
+# integer work not counted):
+#   B1 = ln + radius + sincos + 2 outputs                                   = 31
+#   B2 = ln + radius + sincos16 + 2                                         = 38
+#   B3 = bulk pair (m^2 1, Moebius 2, div 8, Horner 15, r 2, A 1, sincos16 21, 2) 52;
+#        tail pair (1/9): 1 - m^2 1 + ln 8 + rsqrt 5 + r 2 replace 27 of it  = 52 - 11/9
+#   P  = (4/pi) candidates x 3 (s) + per accepted pair ln 8 + hs 1 + rsqrt 5 + r 2 + 2 = 12/pi + 18
+DP_PER_PAIR = {"B1": 31.0, "B2": 38.0, "B3": 52.0 - 11.0 / 9.0, "P": 12.0 / math.pi + 18.0}
 FP64_PEAK_NOMINAL = 148 * 64 * 1.965e9  # SMs x FP64 lanes per SM x max SM clock = DP instr/s
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
 # capture of the same launch (profiles/); None until captured.
@@ -337,7 +339,7 @@ def main():
                         "unit": "GB/s", "frac": t_hbm / t, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
         roofs[m]["traffic"] = None
     dom = max(METHODS, key=lambda m: per_ms[m])
-    kname = "polar_kernel" if dom == "P" else "bm_kernel<%s>" % dom[1]
+    kname = {"P": "polar_kernel<20,1>", "B3": "b3_kernel<24>"}.get(dom, "bm_kernel<%s,20>" % dom[1:])
     roof = dict(roofs[dom], kernel="%s (%s)" % (kname, dom), method=dom)
     roof["traffic"] = TRAFFIC.get(dom)
 
