@@ -100,9 +100,19 @@ enum class Kind { BM1, BM2, BM3, POLAR, POLAR2, UNIFORM };
 
 template <int V>
 void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
-    if (V == 3 && p.aligned && p.log2E == 0 && ns >= (uint32_t)(kTriWarps * h->num_sms))
-        b3_kernel<kTriWarps><<<h->num_sms, kTriWarps * 32, tri_smem(kTriWarps), st>>>(p);
-    else if (ns >= (uint32_t)(kBigBlock * h->num_sms))
+    const bool plain = p.aligned && p.log2E == 0;
+    if constexpr (V == 3) {
+        if (plain && ns >= (uint32_t)(kTriWarps * h->num_sms)) {
+            b3_kernel<kTriWarps><<<h->num_sms, kTriWarps * 32, tri_smem(kTriWarps), st>>>(p);
+            return;
+        }
+    } else {
+        if (plain && ns >= (uint32_t)(kPwWarps * h->num_sms)) {
+            pw_kernel<V, kPwWarps><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
+            return;
+        }
+    }
+    if (ns >= (uint32_t)(kBigBlock * h->num_sms))
         bm_kernel<V, kBigBlock><<<h->num_sms, kBigBlock * 32, bm_smem(kBigBlock), st>>>(p);
     else
         bm_kernel<V, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.bm[V], h->num_sms), kWarpsPerBlock * 32,
@@ -111,7 +121,9 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
 
 template <int M>
 void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
-    if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
+    if (M == 1 && p.aligned && p.log2E == 0 && p.q + 1 < (1ull << 31) && ns >= (uint32_t)(kPwWarps * h->num_sms))
+        pw_kernel<4, kPwWarps><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
+    else if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
         polar_kernel<kBigBlockPolar, M><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
     else
         polar_kernel<kWarpsPerBlock, M><<<grid_for(ns, kWarpsPerBlock, h->occ.polar, h->num_sms),
@@ -258,6 +270,9 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(bm_kernel<2, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(bm_kernel<3, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(b3_kernel<kTriWarps>, kTriWarps, tri_smem(kTriWarps));
+    occupancy(pw_kernel<1, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(pw_kernel<2, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(pw_kernel<4, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
     occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     occupancy(polar_kernel<kBigBlockPolar, 2>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     h->occ.uni = occupancy(uniform_kernel, kWarpsPerBlock, kUniSmem);

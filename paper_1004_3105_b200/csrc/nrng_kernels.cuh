@@ -467,11 +467,16 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 const uint32_t nb = (ph + 1) & 3;
                 uint64_t g[kBlkW];
                 phase_gen_load(bl, nb, g);
+#ifndef NRNG_EXP_P_NOCONSUME
 #pragma unroll
                 for (int u = 0; u < kPU; ++u) {
                     const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(L.buf + kBlk * ph + 64 * u + 2 * lane);
                     ok[u] = polar_candidate(w.x, w.y, c[u]);
                 }
+#else  // experiment: candidates from the freshly generated words (no window re-read; wrong stream order)
+#pragma unroll
+                for (int u = 0; u < kPU; ++u) ok[u] = polar_candidate(g[2 * u], g[2 * u + 1], c[u]);
+#endif
                 bool stop;
                 const uint32_t used = polar_rank(ok, m, cnt - acc, lt, stop);
                 if (!stop) phase_gen_store(bl, nb, g);
@@ -546,6 +551,308 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
         }
         lfg_store(L, rk, C, lane);
         if (lane == 0) p.count[k] = C + (L.wc - kW0);
+        __syncwarp();
+    }
+}
+
+// ------------------------------------------------------------------ swizzled pair window
+// B1, B2, P and P2 consume the stream in word pairs (x_{2i}, x_{2i+1}).  Here each lane
+// GENERATES the pair it consumes, from four 64-bit loads (the sources x_{w-607}, x_{w-606},
+// x_{w-273}, x_{w-272} of an even w start at odd positions, so they are two unaligned
+// pairs), stores it with two 64-bit stores and transforms it from registers: no consumer
+// re-read, no shuffle.  A lane stride of 2 words would put lanes l and l+8 of a half-warp
+// on the same bank pair; the window is therefore XOR-swizzled, logical position p held at
+// physical word swz(p) = p ^ ((p >> 4) & 1) (bit 0 flipped in every other 16-word row),
+// which makes every stride-2 half-warp access hit 16 distinct bank pairs, keeps each
+// aligned pair inside its 16-byte slot and keeps contiguous 32-word accesses a
+// permutation of their row.  Because the per-lane part of every address (2l + a constant
+// whose low 6 bits are fixed) is the same in every row, the swizzle is six per-lane
+// offsets computed once; rows only add a uniform multiple of 64.  Window: 1024 words +
+// the 256-word mirror of positions [0, 256) (sources of a row run up to 63 words past
+// the end).  Word i of the call (i < 0: the loaded state) is at logical position i mod 1024.
+// Used for aligned, plain-layout calls filling the GPU; the rest go to bm_kernel /
+// polar_kernel.  M: 1 = B1, 2 = B2, 4 = P (P2 keeps polar_kernel: here it spilled).
+constexpr int kPwWarps = 20;
+__device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
+
+struct PwLane {  // physical offsets of this lane's words in a row whose base is 0
+    uint32_t a0, a1, b0, b1, d0, d1;
+};
+__device__ __forceinline__ PwLane pw_lane(int lane) {
+    const uint32_t l2 = 2 * lane;
+    return PwLane{swz(kWin - kLagR + l2), swz(kWin - kLagR + 1 + l2), swz(kWin - kLagS + l2),
+                  swz(kWin - kLagS + 1 + l2), swz(l2), swz(l2 + 1)};
+}
+
+// Generate R consecutive pair rows starting at logical row base K (a multiple of 64 below
+// 1024; rows at K + 64 t must not cross 1024): lane l makes (x_{K+64t+2l}, x_{K+64t+2l+1}).
+// The source runs are masked once per call (a run of R rows may extend up to 255 words past
+// 1023, into the mirror), so every row is the same four per-lane pointers plus an immediate.
+// All loads are issued before any store (all sources are older than the rows: 64 R <= 273).
+template <int R>
+__device__ __forceinline__ void pw_gen(uint64_t* buf, uint32_t K, const PwLane& o, uint64_t (&w0)[R],
+                                       uint64_t (&w1)[R]) {
+    static_assert(64 * R <= kLagS && 64 * R <= kMirror, "rows of one call must be independent");
+    const int ka = (int)((K + (kWin - kLagR)) & kWinMask) - (kWin - kLagR);  // multiple of 64
+    const int kb = (int)((K + (kWin - kLagS)) & kWinMask) - (kWin - kLagS);
+    const uint64_t* pa0 = buf + (ka + (int)o.a0);
+    const uint64_t* pa1 = buf + (ka + (int)o.a1);
+    const uint64_t* pb0 = buf + (kb + (int)o.b0);
+    const uint64_t* pb1 = buf + (kb + (int)o.b1);
+    uint64_t a0[R], a1[R], b0[R], b1[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        a0[t] = pa0[64 * t];
+        a1[t] = pa1[64 * t];
+        b0[t] = pb0[64 * t];
+        b1[t] = pb1[64 * t];
+    }
+    uint64_t* pd0 = buf + (K + o.d0);
+    uint64_t* pd1 = buf + (K + o.d1);
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        w0[t] = a0[t] + b0[t];
+        w1[t] = a1[t] + b1[t];
+        pd0[64 * t] = w0[t];
+        pd1[64 * t] = w1[t];
+    }
+    if (K < (uint32_t)kMirror) {  // rows in [0, 256): mirrored at +1024
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            pd0[kWin + 64 * t] = w0[t];
+            pd1[kWin + 64 * t] = w1[t];
+        }
+    }
+}
+
+// The same for a block at a compile-time base K (the steady loops are unrolled over the 4
+// block positions): every address is a per-lane pointer plus an immediate.
+struct PwPtrs {
+    const uint64_t *a0, *a1, *b0, *b1;
+    uint64_t *d0, *d1;
+};
+__device__ __forceinline__ PwPtrs pw_ptrs(uint64_t* buf, const PwLane& o) {
+    return PwPtrs{buf + o.a0, buf + o.a1, buf + o.b0, buf + o.b1, buf + o.d0, buf + o.d1};
+}
+template <int R, int K>
+__device__ __forceinline__ void pw_gen_c(const PwPtrs& pp, uint64_t (&w0)[R], uint64_t (&w1)[R]) {
+    static_assert(64 * R <= kLagS && 64 * R <= kMirror && K % 64 == 0 && K + 64 * R <= kWin, "row geometry");
+    constexpr int ka = ((K + (kWin - kLagR)) & kWinMask) - (kWin - kLagR);
+    constexpr int kb = ((K + (kWin - kLagS)) & kWinMask) - (kWin - kLagS);
+    uint64_t a0[R], a1[R], b0[R], b1[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        a0[t] = pp.a0[ka + 64 * t];
+        a1[t] = pp.a1[ka + 64 * t];
+        b0[t] = pp.b0[kb + 64 * t];
+        b1[t] = pp.b1[kb + 64 * t];
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        w0[t] = a0[t] + b0[t];
+        w1[t] = a1[t] + b1[t];
+        pp.d0[K + 64 * t] = w0[t];
+        pp.d1[K + 64 * t] = w1[t];
+        if (K < kMirror) {
+            pp.d0[K + kWin + 64 * t] = w0[t];
+            pp.d1[K + kWin + 64 * t] = w1[t];
+        }
+    }
+}
+
+// Source-run offsets (words, relative to the per-lane pointers) of the block at position
+// 256 ph: a warp-uniform constant-bank load per block instead of per-block mask arithmetic.
+__constant__ int2 kPwPhaseOff[4] = {
+    {((0 + (kWin - kLagR)) & kWinMask) - (kWin - kLagR), ((0 + (kWin - kLagS)) & kWinMask) - (kWin - kLagS)},
+    {((256 + (kWin - kLagR)) & kWinMask) - (kWin - kLagR), ((256 + (kWin - kLagS)) & kWinMask) - (kWin - kLagS)},
+    {((512 + (kWin - kLagR)) & kWinMask) - (kWin - kLagR), ((512 + (kWin - kLagS)) & kWinMask) - (kWin - kLagS)},
+    {((768 + (kWin - kLagR)) & kWinMask) - (kWin - kLagR), ((768 + (kWin - kLagS)) & kWinMask) - (kWin - kLagS)}};
+template <int R>
+__device__ __forceinline__ void pw_gen_r(const PwPtrs& pp, uint32_t ph, uint64_t (&w0)[R], uint64_t (&w1)[R]) {
+    static_assert(64 * R <= kLagS && 64 * R <= kMirror, "row geometry");
+    const int2 kk = kPwPhaseOff[ph];
+    const int K = (int)(kBlk * ph);
+    uint64_t a0[R], a1[R], b0[R], b1[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        a0[t] = pp.a0[kk.x + 64 * t];
+        a1[t] = pp.a1[kk.x + 64 * t];
+        b0[t] = pp.b0[kk.y + 64 * t];
+        b1[t] = pp.b1[kk.y + 64 * t];
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        w0[t] = a0[t] + b0[t];
+        w1[t] = a1[t] + b1[t];
+        pp.d0[K + 64 * t] = w0[t];
+        pp.d1[K + 64 * t] = w1[t];
+    }
+    if (ph == 0) {
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            pp.d0[kWin + 64 * t] = w0[t];
+            pp.d1[kWin + 64 * t] = w1[t];
+        }
+    }
+}
+
+// One steady-state B1/B2 block (128 pairs) at compile-time window base K.
+template <int M, int K>
+__device__ __forceinline__ void pw_bm_block(const PwPtrs& pp, const TParams& tp, const Tables& tab, double2* o) {
+    uint64_t wu[4], wv[4];
+    pw_gen_c<4, K>(pp, wu, wv);
+    double x[4], y[4];
+    if (M == 1)
+        b1_pairs<4>(wu, wv, tp, tab, x, y);
+    else
+        b2_pairs<4>(wu, wv, tp, tab, x, y);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+    __syncwarp();
+}
+
+// One Polar step (128 candidates, one block) at compile-time base K; returns whether the
+// quota was reached (exact stop: `used` = candidates consumed of this block).
+template <int M, int K>
+__device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& tp, const Tables& tab,
+                                               const BulkParams& p, const Quota& qk, double2* o, bool direct,
+                                               uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt) {
+    uint64_t wa[kPU], wb[kPU];
+    pw_gen_c<kPU, K>(pp, wa, wb);
+    PolarCand c[kPU];
+    bool ok[kPU];
+    unsigned m[kPU];
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) ok[u] = polar_candidate(wa[u], wb[u], c[u]);
+    bool stop;
+    used = polar_rank(ok, m, cnt - acc, lt, stop);
+    double ox[kPU], oy[kPU];
+    if (M == 5)
+        p2_transform<kPU>(c, tp, tab, ox, oy);
+    else
+        polar_transform<kPU>(c, tp, tab, ox, oy);
+    if (direct) {
+#pragma unroll
+        for (int u = 0; u < kPU; ++u) {
+            if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), make_double2(ox[u], oy[u]));
+            acc += __popc(m[u]);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < kPU; ++u) {
+            if ((m[u] >> lane) & 1u)
+                store_pair(p.out, 2 * (qk.off + acc + __popc(m[u] & lt)), p.shift, p.n, ox[u], oy[u], true);
+            acc += __popc(m[u]);
+        }
+    }
+    __syncwarp();
+    return stop;
+}
+
+template <int M, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
+    extern __shared__ __align__(16) uint64_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
+    __syncthreads();
+    uint64_t* const buf = smem + warp * kWinAlloc;
+    const PwLane ol = pw_lane(lane);
+    const PwPtrs pp = pw_ptrs(buf, ol);
+    const unsigned lt = lanemask_lt(lane);
+    for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
+        const Quota qk = quota(p.q, p.rem, k);
+        if (qk.cnt == 0) continue;
+        const uint64_t C = p.count[k];
+        uint64_t* rk = p.ring + (uint64_t)k * kPitch;
+        {   // x_{C-607+j} -> logical position 417 + j
+            const uint32_t base = (uint32_t)(C % kLagR);
+            for (int j = lane; j < kLagR; j += 32) {
+                uint32_t q = base + j;
+                q = q >= (uint32_t)kLagR ? q - kLagR : q;
+                buf[swz((kWin - kLagR) + j)] = rk[q];
+            }
+        }
+        __syncwarp();
+        uint64_t used;  // words consumed by this call
+        if constexpr (M <= 2) {
+            // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
+            const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
+            const uint32_t nblk = (uint32_t)(safe_cnt / 128);
+            double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
+            uint32_t b = 0;
+            // B2: unrolled over the 4 block positions (compile-time window offsets); B1: one
+            // block body with the offsets from the constant bank (measured faster for B1: the
+            // unrolled body issued 16% fewer instructions but scheduled worse, 79% vs 92% of
+            // the issue bound)
+            if constexpr (M == 2) while (b < nblk) {  // 4 block positions per pass, compile-time window offsets
+                pw_bm_block<M, 0>(pp, p.tp, tab, o);
+                o += 128;
+                if (++b == nblk) break;
+                pw_bm_block<M, 256>(pp, p.tp, tab, o);
+                o += 128;
+                if (++b == nblk) break;
+                pw_bm_block<M, 512>(pp, p.tp, tab, o);
+                o += 128;
+                if (++b == nblk) break;
+                pw_bm_block<M, 768>(pp, p.tp, tab, o);
+                o += 128;
+                ++b;
+            }
+            else for (; b < nblk; ++b, o += 128) {
+                uint64_t wu[4], wv[4];
+                pw_gen_r<4>(pp, b & 3, wu, wv);
+                double x[4], y[4];
+                if (M == 1)
+                    b1_pairs<4>(wu, wv, p.tp, tab, x, y);
+                else
+                    b2_pairs<4>(wu, wv, p.tp, tab, x, y);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+                __syncwarp();
+            }
+            uint32_t K = (256 * b) & kWinMask;
+            for (uint64_t j0 = 128ull * b; j0 < qk.cnt; j0 += 32) {  // last rows, partial, unsafe pair
+                uint64_t wu[1], wv[1];
+                pw_gen<1>(buf, K, ol, wu, wv);
+                double x[1], y[1];
+                if (M == 1)
+                    b1_pairs<1>(wu, wv, p.tp, tab, x, y);
+                else
+                    b2_pairs<1>(wu, wv, p.tp, tab, x, y);
+                if ((uint64_t)lane < qk.cnt - j0)
+                    store_pair(p.out, 2 * (qk.off + j0 + lane), p.shift, p.n, x[0], y[0], true);
+                __syncwarp();
+                K = (K + 64) & kWinMask;
+            }
+            used = 2 * qk.cnt;
+        } else {
+            // Polar: 128 candidates (one 4-row block) per step, ranked by ballot, exact stop (R5).
+            const bool direct = 2 * (qk.off + qk.cnt) <= p.n;
+            double2* const o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift));
+            const uint32_t cnt = (uint32_t)qk.cnt;
+            uint32_t acc = 0, blocks = 0, usedc = 0;
+            for (;;) {
+                if (pw_polar_block<M, 0>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_polar_block<M, 256>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_polar_block<M, 512>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_polar_block<M, 768>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+            }
+            used = (uint64_t)kBlk * blocks + 2 * usedc;
+        }
+        // write back the last min(used, 607) consumed words (word i at logical i mod 1024)
+        const uint32_t nw = used < (uint64_t)kLagR ? (uint32_t)used : (uint32_t)kLagR;
+        const uint32_t pos0 = (uint32_t)((used - nw) & kWinMask);
+        const uint32_t slot0 = (uint32_t)((C + used - nw) % kLagR);
+        for (uint32_t j = lane; j < nw; j += 32) {
+            uint32_t q = slot0 + j;
+            q = q >= (uint32_t)kLagR ? q - kLagR : q;
+            rk[q] = buf[swz((pos0 + j) & kWinMask)];
+        }
+        if (lane == 0) p.count[k] = C + used;
         __syncwarp();
     }
 }
