@@ -250,17 +250,18 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
 // them from registers.  A 64-bit access at a 3-word lane stride is bank-conflict-free (the
 // 16 lanes of a half-warp hit bank pairs 6l mod 32, all distinct), so a row costs 6 loads
 // and 3 stores of 256 B each: 24 B of shared traffic per word, against 34 B for a
-// word-wise refill plus the consumer's re-read.  The window is 9 rows (864 words >= 607
-// + the 2 rows of an iteration) plus a 2-row mirror of rows 0-1 for the sources that run
-// past its end (8.25 KB per warp, 24 warps per SM).  Word i of the call (i < 0: the
-// loaded state) sits at window position i mod 864.
+// word-wise refill plus the consumer's re-read.  An iteration makes 4 rows (128 pairs) in
+// two halves of 2 rows (rows 2-3 read rows 0-1 at lag 273, so a __syncwarp separates the
+// halves).  The window is 11 rows (1056 words >= 607 + the 4 rows of an iteration) plus a
+// 2-row mirror of rows 0-1 for the sources that run past its end (9.75 KB per warp).
+// Word i of the call (i < 0: the loaded state) sits at window position i mod 1056.
 constexpr int kTriRow = 96;
-constexpr int kTriWin = 9 * kTriRow;
+constexpr int kTriWin = 11 * kTriRow;
 constexpr int kTriMirror = 2 * kTriRow;
 constexpr int kTriAlloc = kTriWin + kTriMirror;
 constexpr int kTriScratch = 32;  // per-warp tail-compaction slots (doubles)
-constexpr int kTriWarps = 24;
-static_assert(kTriWin >= kLagR + 2 * kTriRow && kTriRow < kLagS, "triple-row window");
+constexpr int kTriWarps = 20;
+static_assert(kTriWin >= kLagR + 4 * kTriRow && 2 * kTriRow < kLagS, "triple-row window");
 constexpr size_t tri_smem(int nw) {
     return (size_t)nw * (kTriAlloc + kTriScratch) * sizeof(uint64_t) + kTabBytes;
 }
@@ -338,19 +339,27 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         __syncwarp();
         // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
         const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
-        const uint64_t full2 = safe_cnt - safe_cnt % 64;
+        const uint64_t full4 = safe_cnt - safe_cnt % 128;
         double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
         TriPos ps{0, kTriWin - kLagR, kTriWin - kLagS};
         uint64_t j0 = 0;
-        for (; j0 < full2; j0 += 64, o += 64) {
-            uint64_t w1[2], w2[2], w3[2];
-            gen_tri_rows<2>(buf, ps, lane, w1, w2, w3);
-            double x[2], y[2];
-            b3_pairs_compact<2>(w1, w2, w3, p.tp, tab, scr, lane, lt, x, y);
-            __stcs(o, make_double2(x[0], y[0]));
-            __stcs(o + 32, make_double2(x[1], y[1]));
+        for (; j0 < full4; j0 += 128, o += 128) {
+            uint64_t w1[4], w2[4], w3[4];
+            {
+                uint64_t v1[2], v2[2], v3[2];
+                gen_tri_rows<2>(buf, ps, lane, v1, v2, v3);
+                w1[0] = v1[0], w2[0] = v2[0], w3[0] = v3[0], w1[1] = v1[1], w2[1] = v2[1], w3[1] = v3[1];
+                __syncwarp();  // rows 2-3 read rows 0-1 (lag 273)
+                ps.advance(2);
+                gen_tri_rows<2>(buf, ps, lane, v1, v2, v3);
+                w1[2] = v1[0], w2[2] = v2[0], w3[2] = v3[0], w1[3] = v1[1], w2[3] = v2[1], w3[3] = v3[1];
+                ps.advance(2);
+            }
+            double x[4], y[4];
+            b3_pairs_compact<4>(w1, w2, w3, p.tp, tab, scr, lane, lt, x, y);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
             __syncwarp();
-            ps.advance(2);
         }
         for (; j0 < qk.cnt; j0 += 32) {  // the last rows, possibly partial, and the unsafe pair
             uint64_t w1[1], w2[1], w3[1];
