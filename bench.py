@@ -339,7 +339,7 @@ def main():
                         "unit": "GB/s", "frac": t_hbm / t, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
         roofs[m]["traffic"] = None
     dom = max(METHODS, key=lambda m: per_ms[m])
-    kname = {"P": "polar_kernel<20,1>", "B3": "b3_kernel<24>"}.get(dom, "bm_kernel<%s,20>" % dom[1:])
+    kname = {"B1": "pw_kernel<1,20>", "B2": "pw_kernel<2,20>", "B3": "b3_kernel<20>", "P": "pw_kernel<4,20>"}[dom]
     roof = dict(roofs[dom], kernel="%s (%s)" % (kname, dom), method=dom)
     roof["traffic"] = TRAFFIC.get(dom)
 
