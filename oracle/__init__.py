@@ -68,6 +68,8 @@ def lib():
             "orc_normal_polar2": ([p, u32, p, u64, dbl, dbl], C.c_int),
             "orc_polar2_pair": ([dbl, dbl, dbl, dbl, p, p], C.c_int),
             "orc_polar_mask": ([p, u32, p, u64], None),
+            "orc_ratio_candidate": ([dbl, dbl, p], C.c_int),
+            "orc_normal_ratio": ([p, u32, p, u64, dbl, dbl, p], C.c_int),
             "orc_transform_from_uniforms": ([p, u64, p, p, dbl, dbl, C.c_int], C.c_int),
             "orc_stats": ([p, u64, dbl, p, C.c_int, p, p], None),
         }
@@ -149,6 +151,15 @@ class Streams:
         lib().orc_normal_polar2(_ptr(self.st), self.S, _ptr(out), n, mu, sigma)
         return out
 
+    def normal_ratio(self, n: int, mu: float = 0.0, sigma: float = 1.0) -> np.ndarray:
+        """Algorithm R: n normals, one per accepted candidate, stream-major with
+        exact stop; self.ratio_margin = min |a - b|/b over all candidates drawn (reading R27)."""
+        out = np.empty(n, np.float64)
+        mg = np.empty(1, np.float64)
+        lib().orc_normal_ratio(_ptr(self.st), self.S, _ptr(out), n, mu, sigma, _ptr(mg))
+        self.ratio_margin = float(mg[0])
+        return out
+
     def polar_mask(self, cand_per_stream: int) -> np.ndarray:
         m = np.empty(self.S * cand_per_stream, np.uint8)
         lib().orc_polar_mask(_ptr(self.st), self.S, _ptr(m), cand_per_stream)
@@ -201,8 +212,16 @@ def polar2_pair(a, b, mu=0.0, sigma=1.0):
     return bool(acc), ((float(xy[0]), float(xy[1])) if acc else None), tuple(float(t) for t in xys)
 
 
+def ratio_candidate(u, v):
+    """Algorithm R steps 2-3 on one (u, v): (accepted, x, a = x^2, b = -4 ln(1-u)); reject iff a > b."""
+    xab = np.empty(3)
+    acc = lib().orc_ratio_candidate(u, v, _ptr(xab))
+    return bool(acc), float(xab[0]), float(xab[1]), float(xab[2])
+
+
 def transform_from_uniforms(u: np.ndarray, method: int, mu=0.0, sigma=1.0):
-    """method 1/2/3 = B1/B2/B3, 4 = Polar, 5 = P2.  Returns (out[2*pairs], mask or None)."""
+    """method 1/2/3 = B1/B2/B3, 4 = Polar, 5 = P2, 6 = R (out[2j] = sigma x + mu or NaN,
+    out[2j+1] = x).  Returns (out[2*pairs], mask or None)."""
     u = np.ascontiguousarray(u, np.float64)
     per = 3 if method == 3 else 2
     npairs = u.size // per

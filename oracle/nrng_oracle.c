@@ -28,6 +28,9 @@
  *                 r = sigma sqrt(-2 ln(s)/s), return r x + mu, r y + mu.
  *   P2  P:367-385 as P, but s > 8/9 -> r = sigma sqrt(-ln(1-s)/s), else r = sigma h(v(s));
  *                 return x r sqrt2 + mu, y r sqrt2 + mu.
+ *   R   P:421-427 (the ratio method, Algorithm R): x = sqrt(8/e)(v - 1/2)/(1 - u), reject
+ *                 if x^2 > -4 ln(1-u) (the printed "-x^2 ln(1-u) > 4" is an erratum,
+ *                 reading R25), return sigma x + mu -- ONE normal per accepted candidate.
  * Work partition (stream-major, exact-stop; R5/R18): P = ceil(n/2) pairs,
  * stream k yields p_k = q + [k < rem] pairs at out[off_k + 2j], off_k = 2(kq+min(k,rem)).
  */
@@ -373,6 +376,54 @@ int orc_normal_polar2(orc_stream* st, uint32_t S, double* out, uint64_t n, doubl
     return 0;
 }
 
+/* Algorithm R, readings R24-R27: C8E = RN(sqrt(8/e));
+ * x = RN(RN(C8E (v - 1/2)) / (1 - u)) (v - 1/2 and 1 - u exact, left to right as written);
+ * step 3 with the erratum read as the Kinderman-Monahan test (R25): with a = RN(x x) and
+ * b = -4 log(1 - u) (the factor 4 is exact), reject iff a > b; output fma(sigma, x, mu).
+ * As printed, "-x^2 ln(1-u) > 4", the test accepts 76% of the candidates instead of the
+ * sqrt(pi e)/4 = 73.1% that the paper's own 8/sqrt(pi e) = 2.74 uniforms per normal
+ * implies, and its output is not normal (tests/test_oracle_ratio.py).  `ab` receives (a, b). */
+static const double ORC_C8E = 0x1.b72cd3f331398p+0; /* RN(sqrt(8/e)) = 1.7155277699214136 */
+static int ratio_candidate(double u, double v, double* x, double* ab) {
+    *x = (ORC_C8E * (v - 0.5)) / (1.0 - u);
+    ab[0] = *x * *x;
+    ab[1] = -4.0 * log(1.0 - u);
+    return !(ab[0] > ab[1]);
+}
+/* xab = (x, a, b) */
+int orc_ratio_candidate(double u, double v, double* xab) { return ratio_candidate(u, v, &xab[0], &xab[1]); }
+
+/* Algorithm R with exact stop (reading R5 with normals as the unit, R26): stream k draws
+ * candidates until its quota of n/S (+1 for k < n mod S) normals is accepted, one normal
+ * per accepted candidate at out[off_k + j].  *margin (if given) receives the smallest
+ * |a - b| / b over every candidate drawn with b > 0 (b = 0 means u = 0, where ln is
+ * exactly 0 everywhere): how close the closest accept decision came to depending on the
+ * last bits of the logarithm, which the GPU parity tests check (reading R27). */
+int orc_normal_ratio(orc_stream* st, uint32_t S, double* out, uint64_t n, double mu, double sigma, double* margin) {
+    double mg = INFINITY;
+#pragma omp parallel for schedule(static) reduction(min : mg)
+    for (long k = 0; k < (long)S; ++k) {
+        uint64_t cnt, off;
+        quota(n, S, (uint32_t)k, &cnt, &off);
+        uint64_t j = 0;
+        while (j < cnt) {
+            double u = next_uniform(&st[k]);
+            double v = next_uniform(&st[k]);
+            double x, ab[2];
+            int acc = ratio_candidate(u, v, &x, ab);
+            if (ab[1] > 0.0) {
+                double d = fabs(ab[0] - ab[1]) / ab[1];
+                if (d < mg) mg = d;
+            }
+            if (!acc) continue; /* step 3: reject */
+            out[off + j] = fma(sigma, x, mu);
+            ++j;
+        }
+    }
+    if (margin) *margin = mg;
+    return 0;
+}
+
 /* Accept mask of exactly `cand` candidates per stream (2 uniforms each), stream-major. */
 void orc_polar_mask(orc_stream* st, uint32_t S, uint8_t* mask, uint64_t cand) {
 #pragma omp parallel for schedule(static)
@@ -386,18 +437,24 @@ void orc_polar_mask(orc_stream* st, uint32_t S, uint8_t* mask, uint64_t cand) {
     }
 }
 
-/* Transforms on caller-given uniforms: B1/B2/P/P2 use 2 per pair, B3 3 per pair.
- * method: 1,2,3 = B1,B2,B3; 4 = P, 5 = P2 (rejected candidates give NaN, NaN and mask 0). */
+/* Transforms on caller-given uniforms: B1/B2/P/P2/R use 2 per pair, B3 3 per pair.
+ * method: 1,2,3 = B1,B2,B3; 4 = P, 5 = P2 (rejected candidates give NaN, NaN and mask 0);
+ * 6 = R: out[2j] = sigma x + mu (NaN if rejected), out[2j+1] = x (always). */
 int orc_transform_from_uniforms(const double* u, uint64_t n_pairs, double* out, uint8_t* mask, double mu,
                                 double sigma, int method) {
-    if (method < 1 || method > 5) return -1;
+    if (method < 1 || method > 6) return -1;
 #pragma omp parallel for schedule(static)
     for (long j = 0; j < (long)n_pairs; ++j) {
         double x = NAN, y = NAN;
         if (method == 1) b1_pair(u[2 * j], u[2 * j + 1], mu, sigma, &x, &y);
         else if (method == 2) b2_pair(u[2 * j], u[2 * j + 1], mu, sigma, &x, &y);
         else if (method == 3) b3_pair(u[3 * j], u[3 * j + 1], u[3 * j + 2], mu, sigma, &x, &y);
-        else {
+        else if (method == 6) {
+            double ab[2];
+            int acc = ratio_candidate(u[2 * j], u[2 * j + 1], &y, ab);
+            if (mask) mask[j] = (uint8_t)acc;
+            if (acc) x = fma(sigma, y, mu);
+        } else {
             double cx, cy, s;
             int acc = polar_candidate(u[2 * j], u[2 * j + 1], &cx, &cy, &s);
             if (mask) mask[j] = (uint8_t)acc;
