@@ -99,6 +99,16 @@ int nrng_normal_polar(nrng_handle h, double* out, size_t n, double mu, double si
  * y r sqrt2 + mu.  Errors as nrng_normal_polar. */
 int nrng_normal_polar2(nrng_handle h, double* out, size_t n, double mu, double sigma);
 
+/* Algorithm R, the ratio method of Kinderman and Monahan:
+ * for consecutive uniforms (u, v) of a stream, x = RN(RN(sqrt(8/e) (v - 1/2)) / (1 - u));
+ * reject iff RN(x x) > -4 ln(1 - u) (the printed step 3 is an erratum, R25);
+ * accepted candidates give ONE normal each, fma(sigma, x, mu).  Unlike the pair methods the
+ * unit is a normal: stream k yields n/S (+1 for k < n mod S) normals at out[off_k + j],
+ * exact stop (R26), no dropped deviate for odd n.  The step-2.5 pretests are not used (they
+ * change no output, R28).  Uses 8/sqrt(pi e) = 2.74 uniforms per normal on average.
+ * Errors as nrng_normal_polar.  Not available in the sequential mode. */
+int nrng_normal_ratio(nrng_handle h, double* out, size_t n, double mu, double sigma);
+
 /* ---- sequential mode: RANN3-style buffering ----
  * One canonical, partition-invariant sequence per handle and method: epoch e is the output
  * of every stream making E more pairs, stream-major (2 S E deviates; E = epoch_pairs, a
@@ -144,7 +154,9 @@ int nrng_uniform(nrng_handle h, double* out, size_t n);
 int nrng_polar_mask(nrng_handle h, uint8_t* dev_mask, size_t cand_per_stream);
 /* Transforms on caller-given device uniforms (no generator state involved):
  * method 1/2/3 = B1/B2/B3 (2/2/3 uniforms per pair), 4 = Polar candidate, 5 = P2 candidate
- * (2 uniforms; rejected -> NaN outputs and dev_mask 0; dev_mask may be NULL).  out: 2*n_pairs.
+ * (2 uniforms; rejected -> NaN outputs and dev_mask 0; dev_mask may be NULL), 6 = R
+ * candidate (2 uniforms: out[2j] = sigma x + mu, NaN if rejected; out[2j+1] = x).
+ * out: 2*n_pairs.
  * Enqueued on cuda_stream. */
 int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* dev_out, uint8_t* dev_mask,
                                  double mu, double sigma, int method, void* cuda_stream);

@@ -580,7 +580,8 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
 // the 256-word mirror of positions [0, 256) (sources of a row run up to 63 words past
 // the end).  Word i of the call (i < 0: the loaded state) is at logical position i mod 1024.
 // Used for aligned, plain-layout calls filling the GPU; the rest go to bm_kernel /
-// polar_kernel.  M: 1 = B1, 2 = B2, 4 = P (P2 keeps polar_kernel: here it spilled).
+// polar_kernel.  M: 1 = B1, 2 = B2, 4 = P (P2 keeps polar_kernel: here it spilled), 6 = R
+// (Algorithm R, the only path for it besides the tiny-quota kernel).
 constexpr int kPwWarps = 20;
 __device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
 
@@ -758,6 +759,29 @@ __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& 
     return stop;
 }
 
+// One Algorithm R step (128 candidates, one block) at compile-time base K: one normal per
+// accepted candidate, ranked by ballot in candidate order, exact stop (R26).  `o` points at
+// this stream's first output slot.
+template <int K>
+__device__ __forceinline__ bool pw_ratio_block(const PwPtrs& pp, const TParams& tp, const Tables& tab, double* o,
+                                               uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt) {
+    uint64_t wa[kPU], wb[kPU];
+    pw_gen_c<kPU, K>(pp, wa, wb);
+    double x[kPU];
+    bool ok[kPU];
+    unsigned m[kPU];
+    ratio_candidates<kPU>(wa, wb, tab, x, ok);
+    bool stop;
+    used = polar_rank(ok, m, cnt - acc, lt, stop);
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) {
+        if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), __fma_rn(tp.sigma, x[u], tp.mu));
+        acc += __popc(m[u]);
+    }
+    __syncwarp();
+    return stop;
+}
+
 template <int M, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
@@ -834,6 +858,22 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
                 K = (K + 64) & kWinMask;
             }
             used = 2 * qk.cnt;
+        } else if constexpr (M == 6) {
+            // Algorithm R: 128 candidates per step, one normal per accepted candidate (R26).
+            double* const o = p.out + (qk.off - p.shift);
+            const uint32_t cnt = (uint32_t)qk.cnt;
+            uint32_t acc = 0, blocks = 0, usedc = 0;
+            for (;;) {
+                if (pw_ratio_block<0>(pp, p.tp, tab, o, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_ratio_block<256>(pp, p.tp, tab, o, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_ratio_block<512>(pp, p.tp, tab, o, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_ratio_block<768>(pp, p.tp, tab, o, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+            }
+            used = (uint64_t)kBlk * blocks + 2 * usedc;
         } else {
             // Polar: 128 candidates (one 4-row block) per step, ranked by ballot, exact stop (R5).
             const bool direct = 2 * (qk.off + qk.cnt) <= p.n;
@@ -909,7 +949,7 @@ __device__ __forceinline__ void ring_commit(uint64_t* __restrict__ r, uint32_t& 
     a = a >= (uint32_t)kLagR ? a - kLagR : a;
 }
 
-template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2
+template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2; 6 = R (units: normals, one per accept)
 __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
     __shared__ double2 tabs[kTabBytes / 16];
     const Tables tab = load_tables(tabs);
@@ -930,7 +970,28 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
         ring_peek<CW>(r, a, w);
         double x[4], y[4];
         uint32_t take, words;
-        if (V >= 4) {
+        if (V == 6) {
+            uint64_t wu[4], wv[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                wu[t] = w[2 * t];
+                wv[t] = w[2 * t + 1];
+            }
+            double xr[4];
+            bool ok[4];
+            ratio_candidates<4>(wu, wv, tab, xr, ok);
+            uint32_t got = 0, cand = 4;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (ok[t] && j + got < qk.cnt) {
+                    const uint64_t g = qk.off + j + got;
+                    if (g < p.n) p.out[g - p.shift] = __fma_rn(p.tp.sigma, xr[t], p.tp.mu);
+                    if (j + ++got == qk.cnt) cand = t + 1;  // exact stop
+                }
+            }
+            take = got;
+            words = 2 * cand;
+        } else if (V >= 4) {
             PolarCand c[4];
             bool ok[4];
 #pragma unroll
@@ -1067,6 +1128,14 @@ __global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs,
         } else if (method == 3) {
             const uint64_t w1[1] = {word_of(u[3 * j])}, w2[1] = {word_of(u[3 * j + 1])}, w3[1] = {word_of(u[3 * j + 2])};
             b3_pairs<1>(w1, w2, w3, tp, tab, x, y);
+        } else if (method == 6) {
+            const uint64_t wu[1] = {word_of(u[2 * j])}, wv[1] = {word_of(u[2 * j + 1])};
+            double xr[1];
+            bool ok[1];
+            ratio_candidates<1>(wu, wv, tab, xr, ok);
+            if (mask) mask[j] = ok[0] ? 1 : 0;
+            if (ok[0]) x[0] = __fma_rn(tp.sigma, xr[0], tp.mu);
+            y[0] = xr[0];
         } else {
             PolarCand pc[1];
             const bool ok = polar_candidate(word_of(u[2 * j]), word_of(u[2 * j + 1]), pc[0]);

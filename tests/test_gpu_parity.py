@@ -42,6 +42,8 @@ def gen_normals(g, method, n, mu, sigma):
 
 
 def ora_normals(st, method, n, mu, sigma):
+    if method == "R":
+        return st.normal_ratio(n, mu, sigma)
     if method == "P":
         return st.normal_polar(n, mu, sigma)
     if method == "P2":
@@ -225,6 +227,71 @@ def test_transform_from_uniforms(method):
         acc = s < 1
         bulk = np.repeat(s[acc] <= 8 / 9, 2)
         assert np.array_equal(d_out[bulk], o_out[bulk])
+
+
+# ---------------------------------------------------------------- Algorithm R (the ratio method)
+
+def _ratio_margin(u, v):
+    # |a - b| / b of reading R27, recomputed from the definition (b = 0 at u = 0 is exact)
+    x = (float.fromhex("0x1.b72cd3f331398p+0") * (v - 0.5)) / (1.0 - u)
+    b = -4.0 * np.log(1.0 - u)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        return np.where(b > 0, np.abs(x * x - b) / np.where(b > 0, b, 1.0), np.inf)
+
+
+def test_ratio_transform_from_uniforms():
+    u = W.dyadic_uniforms(106, 2 * 400001)
+    e = W.edge_uniforms()
+    u = np.concatenate([np.array([[a, b] for a in e for b in e]).ravel(), u])
+    mu, sigma = -0.75, 1.5
+    d_out, d_mask = P.transform_from_uniforms(torch.from_numpy(u).cuda(), 6, mu, sigma)
+    o_out, o_mask = O.transform_from_uniforms(u, 6, mu, sigma)
+    d_out, d_mask = host(d_out), host(d_mask)
+    # x = RN(RN(C (v - 1/2)) / (1 - u)) uses IEEE operations only: bit-exact everywhere
+    assert np.array_equal(d_out[1::2], o_out[1::2])
+    # the accept decision depends on ln (free to 1 ulp, R27): equal wherever it cannot flip
+    safe = _ratio_margin(u[0::2], u[1::2]) > 1e-12
+    assert safe.mean() > 0.99999
+    assert np.array_equal(d_mask[safe], o_mask[safe])
+    acc = o_mask.astype(bool) & safe
+    assert np.array_equal(d_out[0::2][acc], o_out[0::2][acc])
+    assert np.all(np.isnan(d_out[0::2][~d_mask.astype(bool)]))
+
+
+@pytest.mark.parametrize("S,ns", [(64, [1, 3, 2 * 64 + 1, 64 * 33 + 5, 64 * 700 + 17]),
+                                  (1000, [1000 * 130 + 999, 7]),
+                                  (4160, [4160 * 40 + 2345, 4160 * 3 + 7, 4160 * 129])])
+def test_ratio_bulk_parity(S, ns):
+    # tiny quotas (thread per stream), 4-warp and one-block-per-SM pair-window kernels, with
+    # remainders and consecutive calls; every stream against the oracle, state bit-exact
+    g, st = P.Generator(21, S, first_stream=5), O.Streams(21, S, first_stream=5)
+    for n in ns:
+        d = gen_normals(g, "R", n, -1.0, 2.0)
+        o = ora_normals(st, "R", n, -1.0, 2.0)
+        assert st.ratio_margin > 1e-12  # no decision of this run could depend on ln's last bits
+        assert d.size == n and np.array_equal(d, o), (S, n)
+    assert_state_equal(g, st)
+
+
+def test_ratio_bench_shape_sampled_and_host_output():
+    c = W.C5_SHARD
+    g = P.Generator(c.seed, c.streams)
+    out = torch.empty(c.n, dtype=torch.float64, device="cuda")
+    g.normal("R", out=out)
+    per = c.n // c.streams
+    counts = g.stream_counts()
+    for k in [0, 1, 777, c.streams - 1]:
+        st = O.Streams(c.seed, 1, first_stream=k)
+        o = st.normal_ratio(per)
+        assert st.ratio_margin > 1e-12
+        assert np.array_equal(host(out[k * per:(k + 1) * per]), o)
+        assert counts[k] == st.counts[0]
+    del out
+    # host output (chunked staging, one normal per unit)
+    g1, g2 = P.Generator(3, 2048), P.Generator(3, 2048)
+    h = np.empty((1 << 22) + 5)
+    g1.normal("R", out=h, mu=0.5, sigma=3.0)
+    assert np.array_equal(h, gen_normals(g2, "R", h.size, 0.5, 3.0))
 
 
 # ---------------------------------------------------------------- edge cases of the API

@@ -13,7 +13,7 @@ from paper_1004_3105_b200 import workloads as W  # noqa: E402
 c = W.C5_SHARD
 g = P.Generator(c.seed, c.streams)
 out = torch.empty(c.n, dtype=torch.float64, device="cuda")
-for m in ("B1", "B2", "B3", "P", "P2"):
+for m in (sys.argv[1].split(",") if len(sys.argv) > 1 else ("B1", "B2", "B3", "P", "P2")):
     g.normal(m, out=out)
     torch.cuda.synchronize()
     smi = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,clocks_event_reasons.active",
