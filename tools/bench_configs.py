@@ -18,7 +18,7 @@ import torch  # noqa: E402
 import paper_1004_3105_b200 as P  # noqa: E402
 from paper_1004_3105_b200 import workloads as W  # noqa: E402
 
-HBM = 6548.8e9
+HBM = 6554.6e9  # MEASURED_PEAKS.json hbm_gbs (copy)
 
 
 def time_calls(g, method, n, mu, sigma, out, calls, warm=3, graph=False):
@@ -61,7 +61,7 @@ def main():
     big = torch.empty(1 << 31, dtype=torch.float64, device="cuda")
     for c in (W.C1, W.C2, W.C3):
         g = P.Generator(c.seed, c.streams)
-        for m in c.methods + (("P2",) if c.name == "C2" else ()):
+        for m in c.methods + (("P2", "R") if c.name == "C2" else ()):
             res["%s_%s" % (c.name, m)] = time_calls(g, m, c.n, c.mu, c.sigma, big, args.calls)
         g.close()
     c = W.C4
@@ -77,7 +77,7 @@ def main():
     g.close()
     c = W.C5_SHARD
     g = P.Generator(c.seed, c.streams)
-    for m in c.methods + ("P2",):
+    for m in c.methods + ("P2", "R"):
         res["C5shard_%s" % m] = time_calls(g, m, c.n, c.mu, c.sigma, big, 5)
     print(json.dumps(res, indent=1))
 
