@@ -269,12 +269,17 @@ def main():
             if world > 1:
                 dist.all_reduce(fine)
             gofr = G.ks_ad(fine.cpu().numpy())
+            lag = torch.from_numpy(P.serial_corr(out, CFG.mu, 100)).to(dev)  # lags 0..100
+            if world > 1:
+                dist.all_reduce(lag)
+            serial = G.serial_corr_gate(lag.cpu().numpy(), world * CFG.n)
             sums, hist = sums.cpu().numpy(), hist.cpu().numpy()
             n = world * CFG.n
             v = D.moments(sums, n, CFG.sigma)
             v.update({"chi2": D.chi_square(hist, n), "dof": K - 1, "min": float(sums[4]), "max": float(sums[5]),
                       "ks_d": gofr["ks_d"], "ks_pass": gofr["ks_pass"], "ad_a2": gofr["ad_a2"],
-                      "ad_pass": gofr["ad_pass"]})
+                      "ad_pass": gofr["ad_pass"], "serial_r_max": serial["serial_r_max"],
+                      "serial_lag_max": serial["serial_lag_max"], "serial_pass": serial["serial_pass"]})
             validation[m] = v
 
     # ---- e2e: the same step through the public API with HOST output buffers (pinned),

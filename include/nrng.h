@@ -177,6 +177,15 @@ int nrng_stats(const double* dev_x, size_t n, double center, const double* dev_e
 int nrng_gof_hist(const double* dev_x, size_t n, double mu, double sigma, int log2K, uint32_t* dev_hist,
                   void* cuda_stream);
 
+/* Serial-correlation gate ("serial correlation at lags 1..100
+ * bounded by 4/sqrt(n)"): for d_i = dev_x[i] - center, dev_partial[b*(K+1) + k] =
+ * sum over the i of block b (i in [b*4096, (b+1)*4096), i + k < n) of d_i d_{i+k}, k = 0..K,
+ * 1 <= K <= 127; nrng_serial_corr_blocks(n) blocks.  The host sums the blocks in order
+ * (deterministic) and forms r_k = S_k / S_0 (paper_1004_3105_b200/gof.py).  Written, not
+ * accumulated; enqueued on cuda_stream.  Validation only. */
+int nrng_serial_corr(const double* dev_x, size_t n, double center, int K, double* dev_partial, void* cuda_stream);
+size_t nrng_serial_corr_blocks(size_t n);
+
 #ifdef __cplusplus
 }
 #endif

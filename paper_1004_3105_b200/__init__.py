@@ -34,6 +34,8 @@ SIGNATURES = {
     "nrng_normal_polar": ([_p, _p, _sz, _dbl, _dbl], _int),
     "nrng_normal_polar2": ([_p, _p, _sz, _dbl, _dbl], _int),
     "nrng_normal_ratio": ([_p, _p, _sz, _dbl, _dbl], _int),
+    "nrng_serial_corr": ([_p, _sz, _dbl, _int, _p, _p], _int),
+    "nrng_serial_corr_blocks": ([_sz], _sz),
     "nrng_seq_configure": ([_p, _u32], _int),
     "nrng_normal_seq": ([_p, _p, _sz, _dbl, _dbl, _int], _int),
     "nrng_seq_buffered": ([_p], _sz),
@@ -165,6 +167,14 @@ def nrng_stats(x_ptr, n, center, edges_ptr, K, sums_ptr, hist_ptr, stream) -> No
 
 def nrng_gof_hist(x_ptr, n, mu, sigma, log2K, hist_ptr, stream) -> None:
     _check(lib().nrng_gof_hist(x_ptr, n, mu, sigma, log2K, hist_ptr, stream), "nrng_gof_hist")
+
+
+def nrng_serial_corr(x_ptr, n, center, K, partial_ptr, stream) -> None:
+    _check(lib().nrng_serial_corr(x_ptr, n, center, K, partial_ptr, stream), "nrng_serial_corr")
+
+
+def nrng_serial_corr_blocks(n: int) -> int:
+    return int(lib().nrng_serial_corr_blocks(n))
 
 
 def nrng_last_error() -> int:
@@ -341,6 +351,19 @@ def transform_from_uniforms(u, method: int, mu: float = 0.0, sigma: float = 1.0)
     nrng_transform_from_uniforms(u.data_ptr(), n_pairs, out.data_ptr(), mask.data_ptr() if mask is not None else None,
                                  mu, sigma, method, _stream_ptr(torch))
     return out, mask
+
+
+def serial_corr(x, center: float, K: int = 100):
+    """Device lagged sums S_k = sum_i (x_i - c)(x_{i+k} - c), k = 0..K, summed over blocks in a
+    fixed order (numpy float64 array of K+1)."""
+    torch = _torch()
+    n = x.numel()
+    nb = nrng_serial_corr_blocks(n)
+    part = torch.empty(max(1, nb) * (K + 1), dtype=torch.float64, device=x.device)
+    nrng_serial_corr(x.data_ptr(), n, center, K, part.data_ptr(), _stream_ptr(torch))
+    if nb == 0:
+        return np.zeros(K + 1)
+    return part.view(nb, K + 1).cpu().numpy().sum(axis=0)
 
 
 def stats(x, center: float, edges):

@@ -551,6 +551,20 @@ int nrng_gof_hist(const double* dev_x, size_t n, double mu, double sigma, int lo
     return cuda_err(e);
 }
 
+int nrng_serial_corr(const double* dev_x, size_t n, double center, int K, double* dev_partial, void* cuda_stream) {
+    if (K < 1 || K > kCorrMaxLag || (n > 0 && (!dev_x || !dev_partial)) || !std::isfinite(center))
+        return set_err(NRNG_EINVAL);
+    if (n == 0) return set_err(NRNG_OK);
+    const unsigned blocks = (unsigned)nrng_serial_corr_blocks(n);
+    serial_corr_kernel<<<blocks, 128, 0, (cudaStream_t)cuda_stream>>>(dev_x, n, center, K, dev_partial);
+    return cuda_err(cudaGetLastError());
+}
+
+size_t nrng_serial_corr_blocks(size_t n) {
+    const uint64_t tiles = (n + kCorrTile - 1) / kCorrTile;
+    return (size_t)std::min<uint64_t>(tiles, kCorrGrid);
+}
+
 int nrng_last_error(void) { return g_last; }
 
 const char* nrng_error_string(int code) {

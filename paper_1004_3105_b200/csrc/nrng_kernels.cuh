@@ -1236,4 +1236,42 @@ __global__ void gof_hist_kernel(const double* __restrict__ x, uint64_t n, double
     }
 }
 
+// ------------------------------------------------------------------ serial correlation
+// Lagged products for the serial-correlation gate: tile t
+// covers x[t T, t T + T + K) (minus `center`), staged in shared memory; thread k < K+1 sums
+// d_i d_{i+k} over the tile's i with i + k < n.  Blocks stride over the tiles (a fixed grid
+// of min(#tiles, kCorrGrid) blocks, independent of the device, so the summation order is
+// deterministic) and write partial[b][k]; the host sums the blocks in order.  The shared
+// reads are a broadcast (d_i) and a contiguous run (d_{i+k}).  Validation only.
+constexpr int kCorrTile = 4096;
+constexpr int kCorrMaxLag = 127;
+constexpr unsigned kCorrGrid = 2048;
+__global__ void __launch_bounds__(128) serial_corr_kernel(const double* __restrict__ x, uint64_t n, double center,
+                                                          int K, double* __restrict__ partial) {
+    __shared__ double d[kCorrTile + kCorrMaxLag];
+    const int k = threadIdx.x;
+    const uint64_t tiles = (n + kCorrTile - 1) / kCorrTile;
+    double s0 = 0.0, s1 = 0.0;
+    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint64_t base = t * kCorrTile;
+        __syncthreads();
+        for (int j = threadIdx.x; j < kCorrTile + K; j += blockDim.x) {
+            const uint64_t i = base + j;
+            d[j] = i < n ? x[i] - center : 0.0;  // zero padding past n contributes nothing
+        }
+        __syncthreads();
+        if (k <= K) {
+            const uint64_t left = n - base;
+            const int T = left < (uint64_t)kCorrTile ? (int)left : kCorrTile;
+            int i = 0;
+            for (; i + 1 < T; i += 2) {
+                s0 = __fma_rn(d[i], d[i + k], s0);
+                s1 = __fma_rn(d[i + 1], d[i + 1 + k], s1);
+            }
+            if (i < T) s0 = __fma_rn(d[i], d[i + k], s0);
+        }
+    }
+    if (k <= K) partial[(uint64_t)blockIdx.x * (K + 1) + k] = s0 + s1;
+}
+
 }  // namespace nrng

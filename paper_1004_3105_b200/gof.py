@@ -59,3 +59,17 @@ def ks_ad(hist) -> dict:
     lam = d_edges * math.sqrt(n)
     return {"n": int(n), "bins": K, "ks_d": d_edges, "ks_d_max": d_max, "ks_p": kolmogorov_sf(lam),
             "ks_pass": bool(d_max < KS_CRIT_001 / math.sqrt(n)), "ad_a2": A2, "ad_pass": bool(A2 < AD_CRIT_001)}
+
+
+def serial_corr_gate(sums, n: int, z: float = 4.0) -> dict:
+    """Serial-correlation gate: from S_k = sum_i d_i d_{i+k} (k = 0..K, d = x - c),
+    r_k = (S_k / (n - k)) / (S_0 / n); each |r_k| of independent draws is ~N(0, 1/n), gate
+    |r_k| <= z / sqrt(n) for every lag k = 1..K (z = 4 as the SPEC)."""
+    s = np.asarray(sums, dtype=np.float64)
+    K = s.size - 1
+    k = np.arange(1, K + 1)
+    r = (s[1:] / (n - k)) / (s[0] / n)
+    bound = z / math.sqrt(n)
+    worst = int(np.argmax(np.abs(r))) + 1
+    return {"serial_r_max": float(np.max(np.abs(r))), "serial_lag_max": worst, "serial_bound": bound,
+            "serial_pass": bool(np.all(np.abs(r) <= bound))}

@@ -52,3 +52,29 @@ def test_gates_pass_on_oracle_output_and_fail_on_wrong_laws():
 def test_kolmogorov_sf():
     assert abs(gof.kolmogorov_sf(gof.KS_CRIT_001) - 0.01) < 2e-4
     assert gof.kolmogorov_sf(0.1) == 1.0
+
+
+# ---------------------------------------------------------------- serial correlation
+
+def _lag_sums(x, c, K):
+    d = x - c
+    return np.array([np.dot(d[: d.size - k], d[k:]) for k in range(K + 1)])
+
+
+def test_serial_gate_passes_iid_and_catches_ma1():
+    rng = np.random.default_rng(7)
+    z = rng.standard_normal(1_000_001)
+    n = 1_000_000
+    assert gof.serial_corr_gate(_lag_sums(z[1:], 0.0, 100), n)["serial_pass"]
+    # MA(1): x_i = z_i + 0.05 z_{i-1} has r_1 = 0.05 / 1.0025 ~ 0.0499 >> 4/sqrt(n) = 0.004
+    x = z[1:] + 0.05 * z[:-1]
+    g = gof.serial_corr_gate(_lag_sums(x, 0.0, 100), n)
+    assert not g["serial_pass"] and g["serial_lag_max"] == 1 and abs(g["serial_r_max"] - 0.05 / 1.0025) < 0.005
+
+
+def test_serial_gate_on_oracle_uniform_stream():
+    # serial correlation at lags 1..100 of 10^6 draws of one stream within 4/sqrt(10^6)
+    st = O.Streams(2024, 1)
+    u = st.uniform(1_000_000)
+    g = gof.serial_corr_gate(_lag_sums(u, 0.5, 100), u.size)
+    assert g["serial_pass"], g

@@ -294,6 +294,31 @@ def test_ratio_bench_shape_sampled_and_host_output():
     assert np.array_equal(h, gen_normals(g2, "R", h.size, 0.5, 3.0))
 
 
+# ---------------------------------------------------------------- serial correlation gate
+
+def test_serial_corr_kernel_matches_numpy():
+    from paper_1004_3105_b200 import gof as G
+
+    rng = np.random.default_rng(3)
+    for n, K in [(1_000_003, 100), (4096 * 3 + 17, 127), (50, 100), (1, 5)]:
+        x = rng.standard_normal(n) * 2 + 1
+        d = P.serial_corr(torch.from_numpy(x).cuda(), 1.0, K)
+        dx = x - 1.0
+        ref = np.array([np.dot(dx[: max(0, n - k)], dx[k:]) if k < n else 0.0 for k in range(K + 1)])
+        assert np.allclose(d, ref, rtol=1e-12, atol=1e-9 * max(1.0, abs(ref[0])))
+
+
+@pytest.mark.parametrize("what", ["uniform", "B1", "B3", "P", "R"])
+def test_serial_corr_gate_on_generated_streams(what):
+    from paper_1004_3105_b200 import gof as G
+
+    g = P.Generator(77, 1 << 14)
+    n = 1 << 26
+    x = g.uniform(n) if what == "uniform" else g.normal(what, n)
+    r = G.serial_corr_gate(P.serial_corr(x, 0.5 if what == "uniform" else 0.0, 100), n)
+    assert r["serial_pass"], r
+
+
 # ---------------------------------------------------------------- edge cases of the API
 
 def test_zero_n_is_noop_and_sigma_zero():
