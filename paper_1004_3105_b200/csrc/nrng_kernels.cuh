@@ -339,11 +339,10 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         __syncwarp();
         // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
         const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
-        const uint64_t full4 = safe_cnt - safe_cnt % 128;
-        double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
-        TriPos ps{0, kTriWin - kLagR, kTriWin - kLagS};
-        uint64_t j0 = 0;
-        for (; j0 < full4; j0 += 128, o += 128) {
+        const uint32_t nit = (uint32_t)(safe_cnt / 128);  // full 4-row iterations (a 32-bit count: no
+        double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;  // per-iteration
+        TriPos ps{0, kTriWin - kLagR, kTriWin - kLagS};                                   // 64-bit bound)
+        for (uint32_t it = 0; it < nit; ++it, o += 128) {
             uint64_t w1[4], w2[4], w3[4];
             {
                 uint64_t v1[2], v2[2], v3[2];
@@ -361,7 +360,7 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
             for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
             __syncwarp();
         }
-        for (; j0 < qk.cnt; j0 += 32) {  // the last rows, possibly partial, and the unsafe pair
+        for (uint64_t j0 = 128ull * nit; j0 < qk.cnt; j0 += 32) {  // last rows, partial, unsafe pair
             uint64_t w1[1], w2[1], w3[1];
             gen_tri_rows<1>(buf, ps, lane, w1, w2, w3);
             double x[1], y[1];
