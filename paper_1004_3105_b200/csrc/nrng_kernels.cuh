@@ -360,28 +360,35 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
             for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
             __syncwarp();
         }
-        for (uint64_t j0 = 128ull * nit; j0 < qk.cnt; j0 += 32) {  // last rows, partial, unsafe pair
+        // Re-derive the per-stream values from k (kernel parameters live in the constant
+        // bank): nothing but k, `ps` and `nit` has to stay live across the loop, which kept
+        // the compiler from rematerialising the quota inside every iteration.
+        const Quota qk2 = quota(p.q, p.rem, k);
+        for (uint64_t j0 = 128ull * nit; j0 < qk2.cnt; j0 += 32) {  // last rows, partial, unsafe pair
             uint64_t w1[1], w2[1], w3[1];
             gen_tri_rows<1>(buf, ps, lane, w1, w2, w3);
             double x[1], y[1];
             b3_pairs<1>(w1, w2, w3, p.tp, tab, x, y);
-            if ((uint64_t)lane < qk.cnt - j0)
-                store_pair(p.out, 2 * (qk.off + j0 + lane), p.shift, p.n, x[0], y[0], true);
+            if ((uint64_t)lane < qk2.cnt - j0)
+                store_pair(p.out, 2 * (qk2.off + j0 + lane), p.shift, p.n, x[0], y[0], true);
             __syncwarp();
             ps.advance(1);
         }
-        // write back the last min(3 cnt, 607) consumed words (relative index i at i mod 864)
-        const uint64_t used = 3 * qk.cnt;
+        // write back the last min(3 cnt, 607) consumed words (relative index i at i mod 1056)
+        const uint64_t C2 = p.count[k];
+        uint64_t* rk2 = p.ring + (uint64_t)k * kPitch;
+        const uint64_t used = 3 * qk2.cnt;
         const uint32_t nw = used < (uint64_t)kLagR ? (uint32_t)used : (uint32_t)kLagR;
         const uint32_t pos0 = (uint32_t)((used - nw) % kTriWin);  // used - nw >= 0
-        const uint32_t slot0 = (uint32_t)((C + used - nw) % kLagR);
+        const uint32_t slot0 = (uint32_t)((C2 + used - nw) % kLagR);
         for (uint32_t j = lane; j < nw; j += 32) {
             uint32_t pp = pos0 + j, q = slot0 + j;
             pp = pp >= (uint32_t)kTriWin ? pp - kTriWin : pp;
             q = q >= (uint32_t)kLagR ? q - kLagR : q;
-            rk[q] = buf[pp];
+            rk2[q] = buf[pp];
         }
-        if (lane == 0) p.count[k] = C + used;
+        __syncwarp();  // every lane has read count[k] before lane 0 updates it
+        if (lane == 0) p.count[k] = C2 + used;
         __syncwarp();
     }
 }
