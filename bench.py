@@ -344,7 +344,7 @@ def main():
                         "unit": "GB/s", "frac": t_hbm / t, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
         roofs[m]["traffic"] = None
     dom = max(METHODS, key=lambda m: per_ms[m])
-    kname = {"B1": "pw_kernel<1,20>", "B2": "pw_kernel<2,20>", "B3": "b3_kernel<20>", "P": "pw_kernel<4,20>"}[dom]
+    kname = {"B1": "pw_kernel<1,16>", "B2": "pw_kernel<2,16>", "B3": "b3_kernel<16>", "P": "pw_kernel<4,16>"}[dom]
     roof = dict(roofs[dom], kernel="%s (%s)" % (kname, dom), method=dom)
     roof["traffic"] = TRAFFIC.get(dom)
 

@@ -260,7 +260,10 @@ constexpr int kTriWin = 11 * kTriRow;
 constexpr int kTriMirror = 2 * kTriRow;
 constexpr int kTriAlloc = kTriWin + kTriMirror;
 constexpr int kTriScratch = 32;  // per-warp tail-compaction slots (doubles)
-constexpr int kTriWarps = 20;
+#ifndef NRNG_TRI_WARPS
+#define NRNG_TRI_WARPS 16  // measured: 16 warps (107 registers, no rematerialisation) 5.79 ms, 20 warps (96) 5.94, 12 warps 5.82
+#endif
+constexpr int kTriWarps = NRNG_TRI_WARPS;
 static_assert(kTriWin >= kLagR + 4 * kTriRow && 2 * kTriRow < kLagS, "triple-row window");
 constexpr size_t tri_smem(int nw) {
     return (size_t)nw * (kTriAlloc + kTriScratch) * sizeof(uint64_t) + kTabBytes;
@@ -588,7 +591,10 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
 // Used for aligned, plain-layout calls filling the GPU; the rest go to bm_kernel /
 // polar_kernel.  M: 1 = B1, 2 = B2, 4 = P (P2 keeps polar_kernel: here it spilled), 6 = R
 // (Algorithm R, the only path for it besides the tiny-quota kernel).
-constexpr int kPwWarps = 20;
+#ifndef NRNG_PW_WARPS
+#define NRNG_PW_WARPS 16  // measured (ms per 2^31, B1/B2/P): 16 warps 3.68/3.88/4.52, 12: 4.09/3.83/4.54, 14: 4.28/4.21/4.72, 18: 4.06/4.44/4.73, 20 (another box): 3.79/4.19/4.30
+#endif
+constexpr int kPwWarps = NRNG_PW_WARPS;
 __device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
 
 struct PwLane {  // physical offsets of this lane's words in a row whose base is 0
