@@ -252,11 +252,15 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
 // and 3 stores of 256 B each: 24 B of shared traffic per word, against 34 B for a
 // word-wise refill plus the consumer's re-read.  An iteration makes 4 rows (128 pairs) in
 // two halves of 2 rows (rows 2-3 read rows 0-1 at lag 273, so a __syncwarp separates the
-// halves).  The window is 11 rows (1056 words >= 607 + the 4 rows of an iteration) plus a
-// 2-row mirror of rows 0-1 for the sources that run past its end (9.75 KB per warp).
-// Word i of the call (i < 0: the loaded state) sits at window position i mod 1056.
+// halves).  The window is 12 rows (1152 words >= 607 + the 4 rows of an iteration) plus a
+// 2-row mirror of rows 0-1 for the sources that run past its end (10.5 KB per warp).  12
+// rows are 3 iterations, so the steady loop is unrolled over the 3 iteration phases: every
+// load and store address is the lane's base pointer plus an immediate, and the mirror
+// stores appear in phase 0 only (measured against an 11-row window with runtime positions:
+// the wrap arithmetic and predicated mirror stores were ~5% of the issue slots).
+// Word i of the call (i < 0: the loaded state) sits at window position i mod 1152.
 constexpr int kTriRow = 96;
-constexpr int kTriWin = 11 * kTriRow;
+constexpr int kTriWin = 12 * kTriRow;
 constexpr int kTriMirror = 2 * kTriRow;
 constexpr int kTriAlloc = kTriWin + kTriMirror;
 constexpr int kTriScratch = 32;  // per-warp tail-compaction slots (doubles)
@@ -264,16 +268,17 @@ constexpr int kTriScratch = 32;  // per-warp tail-compaction slots (doubles)
 #define NRNG_TRI_WARPS 16  // measured: 16 warps (107 registers, no rematerialisation) 5.79 ms, 20 warps (96) 5.94, 12 warps 5.82
 #endif
 constexpr int kTriWarps = NRNG_TRI_WARPS;
-static_assert(kTriWin >= kLagR + 4 * kTriRow && 2 * kTriRow < kLagS, "triple-row window");
+static_assert(kTriWin >= kLagR + 4 * kTriRow && 2 * kTriRow < kLagS && kTriWin % (4 * kTriRow) == 0,
+              "triple-row window");
 constexpr size_t tri_smem(int nw) {
     return (size_t)nw * (kTriAlloc + kTriScratch) * sizeof(uint64_t) + kTabBytes;
 }
 
 __device__ __forceinline__ uint32_t tri_wrap(uint32_t x) { return x >= (uint32_t)kTriWin ? x - kTriWin : x; }
 
-// Window positions of an iteration's first row and of its two source runs.
+// Window positions of a row and of its two source runs (the partial last rows of a call).
 struct TriPos {
-    uint32_t d, a, b;  // row 0 at d; sources x_{w-607} at a, x_{w-273} at b (row t at +96 t, via the mirror)
+    uint32_t d, a, b;  // row at d; sources x_{w-607} at a, x_{w-273} at b (row t at +96 t, via the mirror)
     __device__ __forceinline__ void advance(uint32_t rows) {
         d = tri_wrap(d + kTriRow * rows);
         a = tri_wrap(a + kTriRow * rows);
@@ -316,6 +321,54 @@ __device__ __forceinline__ void gen_tri_rows(uint64_t* buf, const TriPos& ps, in
     }
 }
 
+// The two rows 2H, 2H+1 of a steady iteration in phase PH (row 0 at window position
+// 384 PH), at compile-time offsets from the lane's base pointer lb = buf + 3 lane.
+template <int PH, int H>
+__device__ __forceinline__ void gen_tri_half(uint64_t* lb, uint64_t (&w1)[4], uint64_t (&w2)[4], uint64_t (&w3)[4]) {
+    constexpr int d = 4 * kTriRow * PH + 2 * kTriRow * H;
+    constexpr int a = (d + kTriWin - kLagR) % kTriWin, b = (d + kTriWin - kLagS) % kTriWin;
+    static_assert(a + 2 * kTriRow <= kTriAlloc && b + 2 * kTriRow <= kTriAlloc, "source runs inside the mirror");
+    uint64_t sa[2][3], sb[2][3];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            sa[t][i] = lb[a + kTriRow * t + i];
+            sb[t][i] = lb[b + kTriRow * t + i];
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int r = 2 * H + t;
+        w1[r] = sa[t][0] + sb[t][0];
+        w2[r] = sa[t][1] + sb[t][1];
+        w3[r] = sa[t][2] + sb[t][2];
+        lb[d + kTriRow * t] = w1[r];
+        lb[d + kTriRow * t + 1] = w2[r];
+        lb[d + kTriRow * t + 2] = w3[r];
+        if constexpr (d < kTriMirror) {
+            lb[d + kTriWin + kTriRow * t] = w1[r];
+            lb[d + kTriWin + kTriRow * t + 1] = w2[r];
+            lb[d + kTriWin + kTriRow * t + 2] = w3[r];
+        }
+    }
+}
+
+// One steady iteration (4 rows, 128 pairs) in phase PH.
+template <int PH>
+__device__ __forceinline__ void b3_iter(uint64_t* lb, const TParams& tp, const Tables& tab, double* scr, int lane,
+                                        unsigned lt, double2* o) {
+    uint64_t w1[4], w2[4], w3[4];
+    gen_tri_half<PH, 0>(lb, w1, w2, w3);
+    __syncwarp();  // rows 2-3 read rows 0-1 (lag 273)
+    gen_tri_half<PH, 1>(lb, w1, w2, w3);
+    double x[4], y[4];
+    b3_pairs_compact<4>(w1, w2, w3, tp, tab, scr, lane, lt, x, y);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
+    __syncwarp();
+}
+
 // Aligned, plain-layout B3 calls (the dispatcher sends the rest to bm_kernel<3>).
 template <int NW>
 __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
@@ -331,7 +384,7 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
-        {   // x_{C-607+j} -> position 864 - 607 + j
+        {   // x_{C-607+j} -> position 1152 - 607 + j
             const uint32_t base = (uint32_t)(C % kLagR);
             for (int j = lane; j < kLagR; j += 32) {
                 uint32_t q = base + j;
@@ -344,27 +397,23 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
         const uint32_t nit = (uint32_t)(safe_cnt / 128);  // full 4-row iterations (a 32-bit count: no
         double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;  // per-iteration
-        TriPos ps{0, kTriWin - kLagR, kTriWin - kLagS};                                   // 64-bit bound)
-        for (uint32_t it = 0; it < nit; ++it, o += 128) {
-            uint64_t w1[4], w2[4], w3[4];
-            {
-                uint64_t v1[2], v2[2], v3[2];
-                gen_tri_rows<2>(buf, ps, lane, v1, v2, v3);
-                w1[0] = v1[0], w2[0] = v2[0], w3[0] = v3[0], w1[1] = v1[1], w2[1] = v2[1], w3[1] = v3[1];
-                __syncwarp();  // rows 2-3 read rows 0-1 (lag 273)
-                ps.advance(2);
-                gen_tri_rows<2>(buf, ps, lane, v1, v2, v3);
-                w1[2] = v1[0], w2[2] = v2[0], w3[2] = v3[0], w1[3] = v1[1], w2[3] = v2[1], w3[3] = v3[1];
-                ps.advance(2);
-            }
-            double x[4], y[4];
-            b3_pairs_compact<4>(w1, w2, w3, p.tp, tab, scr, lane, lt, x, y);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
-            __syncwarp();
+        uint64_t* const lb = buf + 3 * lane;
+        for (uint32_t it = 0;;) {  // unrolled over the 3 phases of the 12-row window
+            if (it == nit) break;
+            b3_iter<0>(lb, p.tp, tab, scr, lane, lt, o);
+            o += 128;
+            if (++it == nit) break;
+            b3_iter<1>(lb, p.tp, tab, scr, lane, lt, o);
+            o += 128;
+            if (++it == nit) break;
+            b3_iter<2>(lb, p.tp, tab, scr, lane, lt, o);
+            o += 128;
+            ++it;
         }
+        const uint32_t d0 = 4 * kTriRow * (nit % 3);
+        TriPos ps{d0, tri_wrap(d0 + kTriWin - kLagR), tri_wrap(d0 + kTriWin - kLagS)};
         // Re-derive the per-stream values from k (kernel parameters live in the constant
-        // bank): nothing but k, `ps` and `nit` has to stay live across the loop, which kept
+        // bank): nothing but k and `nit` has to stay live across the loop, which kept
         // the compiler from rematerialising the quota inside every iteration.
         const Quota qk2 = quota(p.q, p.rem, k);
         for (uint64_t j0 = 128ull * nit; j0 < qk2.cnt; j0 += 32) {  // last rows, partial, unsafe pair
@@ -377,7 +426,7 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
             __syncwarp();
             ps.advance(1);
         }
-        // write back the last min(3 cnt, 607) consumed words (relative index i at i mod 1056)
+        // write back the last min(3 cnt, 607) consumed words (relative index i at i mod 1152)
         const uint64_t C2 = p.count[k];
         uint64_t* rk2 = p.ring + (uint64_t)k * kPitch;
         const uint64_t used = 3 * qk2.cnt;
@@ -595,6 +644,9 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
 #define NRNG_PW_WARPS 16  // measured (ms per 2^31, B1/B2/P): 16 warps 3.68/3.88/4.52, 12: 4.09/3.83/4.54, 14: 4.28/4.21/4.72, 18: 4.06/4.44/4.73, 20 (another box): 3.79/4.19/4.30
 #endif
 constexpr int kPwWarps = NRNG_PW_WARPS;
+#ifndef NRNG_B1_UNROLL
+#define NRNG_B1_UNROLL 0
+#endif
 __device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
 
 struct PwLane {  // physical offsets of this lane's words in a row whose base is 0
@@ -829,7 +881,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
             // block body with the offsets from the constant bank (measured faster for B1: the
             // unrolled body issued 16% fewer instructions but scheduled worse, 79% vs 92% of
             // the issue bound)
-            if constexpr (M == 2) while (b < nblk) {  // 4 block positions per pass, compile-time window offsets
+            if constexpr (M == 2 || (M == 1 && NRNG_B1_UNROLL)) while (b < nblk) {  // 4 block positions per pass, compile-time window offsets
                 pw_bm_block<M, 0>(pp, p.tp, tab, o);
                 o += 128;
                 if (++b == nblk) break;

@@ -360,6 +360,22 @@ def test_wide_ragged_calls(method):
     assert_state_equal(g, st)
 
 
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P"])
+def test_wide_multi_block_calls_state_continuity(method):
+    # The one-block-per-SM kernels with several steady blocks per stream, ending in every
+    # window phase (B3: 128-pair iterations, 3 phases of its 12-row window; pw kernels:
+    # 128-pair blocks, 4 phases), then a partial row, over consecutive calls: outputs
+    # against the oracle and the written-back state bit-exact after every call.
+    S = 2400
+    g, st = P.Generator(21, S, first_stream=5), O.Streams(21, S, first_stream=5)
+    for pairs in (128 * 4 + 17, 128 * 2 + 5, 128 * 3 + 100, 128 * 5 + 31, 128):
+        n = 2 * S * pairs + 2 * 7
+        d = gen_normals(g, method, n, 0.5, 2.0)
+        o = ora_normals(st, method, n, 0.5, 2.0)
+        assert d.size == n and np.max(np.abs(d - o)) <= tol_for(method), (method, pairs)
+        assert_state_equal(g, st)
+
+
 def test_invalid_arguments():
     g = P.Generator(1, 8)
     out = torch.empty(16, dtype=torch.float64, device="cuda")
