@@ -70,6 +70,8 @@ def lib():
             "orc_polar_mask": ([p, u32, p, u64], None),
             "orc_ratio_candidate": ([dbl, dbl, p], C.c_int),
             "orc_normal_ratio": ([p, u32, p, u64, dbl, dbl, p], C.c_int),
+            "orc_ratio1_pretest": ([dbl, dbl, p], C.c_int),
+            "orc_normal_ratio1": ([p, u32, p, u64, dbl, dbl, p, p], C.c_int),
             "orc_transform_from_uniforms": ([p, u64, p, p, dbl, dbl, C.c_int], C.c_int),
             "orc_stats": ([p, u64, dbl, p, C.c_int, p, p], None),
         }
@@ -160,6 +162,15 @@ class Streams:
         self.ratio_margin = float(mg[0])
         return out
 
+    def normal_ratio1(self, n: int, mu: float = 0.0, sigma: float = 1.0) -> np.ndarray:
+        """Algorithm R1 (R with step 2.5, reading R29): the same output as
+        normal_ratio; self.ratio1_logs / self.ratio1_cands = logarithms evaluated / candidates."""
+        out = np.empty(n, np.float64)
+        nl, nc = np.zeros(1, np.uint64), np.zeros(1, np.uint64)
+        lib().orc_normal_ratio1(_ptr(self.st), self.S, _ptr(out), n, mu, sigma, _ptr(nl), _ptr(nc))
+        self.ratio1_logs, self.ratio1_cands = int(nl[0]), int(nc[0])
+        return out
+
     def polar_mask(self, cand_per_stream: int) -> np.ndarray:
         m = np.empty(self.S * cand_per_stream, np.uint8)
         lib().orc_polar_mask(_ptr(self.st), self.S, _ptr(m), cand_per_stream)
@@ -219,9 +230,17 @@ def ratio_candidate(u, v):
     return bool(acc), float(xab[0]), float(xab[1]), float(xab[2])
 
 
+def ratio1_pretest(u, v):
+    """Algorithm R1 step 2.5 on one (u, v): (class, x, a = x^2); class 1 = P1 (accept without
+    a logarithm), 2 = P2 (reject), 0 = borderline (step 3 decides)."""
+    xa = np.empty(2)
+    cls = lib().orc_ratio1_pretest(u, v, _ptr(xa))
+    return int(cls), float(xa[0]), float(xa[1])
+
+
 def transform_from_uniforms(u: np.ndarray, method: int, mu=0.0, sigma=1.0):
     """method 1/2/3 = B1/B2/B3, 4 = Polar, 5 = P2, 6 = R (out[2j] = sigma x + mu or NaN,
-    out[2j+1] = x).  Returns (out[2*pairs], mask or None)."""
+    out[2j+1] = x), 7 = R1 (as 6; mask = accept | class << 1).  Returns (out[2*pairs], mask or None)."""
     u = np.ascontiguousarray(u, np.float64)
     per = 3 if method == 3 else 2
     npairs = u.size // per

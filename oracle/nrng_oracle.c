@@ -31,6 +31,7 @@
  *   R   P:421-427 (the ratio method, Algorithm R): x = sqrt(8/e)(v - 1/2)/(1 - u), reject
  *                 if x^2 > -4 ln(1-u) (the printed "-x^2 ln(1-u) > 4" is an erratum,
  *                 reading R25), return sigma x + mu -- ONE normal per accepted candidate.
+ *   R1  P:452-468 R with step 2.5 (pretests P1/P2 before the logarithm, reading R29).
  * Work partition (stream-major, exact-stop; R5/R18): P = ceil(n/2) pairs,
  * stream k yields p_k = q + [k < rem] pairs at out[off_k + 2j], off_k = 2(kq+min(k,rem)).
  */
@@ -424,6 +425,63 @@ int orc_normal_ratio(orc_stream* st, uint32_t S, double* out, uint64_t n, double
     return 0;
 }
 
+/* Algorithm R1 = Algorithm R with step 2.5: if P1(u, v), go to step 4 (accept
+ * without a logarithm); else if P2(u, v), reject; else step 3.  The paper only says P1 and
+ * P2 are "easily-computed conditions" whose regions R1 (inside C) and R2 (enclosing C) have
+ * almost the same area, citing Kinderman-Monahan and Leva.  Reading R29: the two
+ * tangent-line bounds of the logarithm, with U = 1 - u and a = x^2 as in step 3:
+ *   ln is concave, so ln U <= ln c + (U - c)/c; at c = e^{-1/4}:  -4 ln U >= 5 - 4 e^{1/4} U;
+ *   ln y <= y - 1 at y = c'/U gives -ln U <= c'/U - 1 - ln c'; at c' = e^{-1.35}:
+ *                                                                -4 ln U <= 4 e^{-1.35}/U + 1.4.
+ * P1: a <= 5 - 4 e^{1/4} U - d;  P2: a >= (4 e^{-1.35} / U)(1 + d) + 1.4 + d,  d = 2^-40.
+ * The margin d (absolute, and relative on the 1/U term) exceeds every rounding error in
+ * these expressions and in step 3's a and b = -4 log U (|b| <= 4 ln 2^53 < 148) by orders
+ * of magnitude, so step 2.5 never decides differently from step 3: R1 returns exactly R's
+ * output, and only the number of logarithms changes.
+ * Returns 1 (P1: accept), 2 (P2: reject) or 0 (borderline: step 3 decides); x and a as in R. */
+static const double ORC_R1_D = 0x1p-40;
+static int ratio1_pretest(double u, double v, double* x, double* a) {
+    *x = (ORC_C8E * (v - 0.5)) / (1.0 - u);
+    *a = *x * *x;
+    const double U = 1.0 - u;
+    if (*a <= 5.0 - 4.0 * exp(0.25) * U - ORC_R1_D) return 1;
+    if (*a >= (4.0 * exp(-1.35) / U) * (1.0 + ORC_R1_D) + 1.4 + ORC_R1_D) return 2;
+    return 0;
+}
+/* xa = (x, a) */
+int orc_ratio1_pretest(double u, double v, double* xa) { return ratio1_pretest(u, v, &xa[0], &xa[1]); }
+
+/* Algorithm R1 with exact stop, the same partition as orc_normal_ratio; *logs (if given)
+ * receives the number of logarithms evaluated (step 3 runs only for borderline candidates),
+ * *cands the number of candidates drawn. */
+int orc_normal_ratio1(orc_stream* st, uint32_t S, double* out, uint64_t n, double mu, double sigma, uint64_t* logs,
+                      uint64_t* cands) {
+    uint64_t nl = 0, nc = 0;
+#pragma omp parallel for schedule(static) reduction(+ : nl, nc)
+    for (long k = 0; k < (long)S; ++k) {
+        uint64_t cnt, off;
+        quota(n, S, (uint32_t)k, &cnt, &off);
+        uint64_t j = 0;
+        while (j < cnt) {
+            double u = next_uniform(&st[k]);
+            double v = next_uniform(&st[k]);
+            double x, a;
+            ++nc;
+            int cls = ratio1_pretest(u, v, &x, &a); /* step 2.5 */
+            if (cls == 2) continue;                  /* P2: reject */
+            if (cls == 0) {                          /* step 3 */
+                ++nl;
+                if (a > -4.0 * log(1.0 - u)) continue;
+            }
+            out[off + j] = fma(sigma, x, mu); /* step 4 */
+            ++j;
+        }
+    }
+    if (logs) *logs = nl;
+    if (cands) *cands = nc;
+    return 0;
+}
+
 /* Accept mask of exactly `cand` candidates per stream (2 uniforms each), stream-major. */
 void orc_polar_mask(orc_stream* st, uint32_t S, uint8_t* mask, uint64_t cand) {
 #pragma omp parallel for schedule(static)
@@ -437,12 +495,13 @@ void orc_polar_mask(orc_stream* st, uint32_t S, uint8_t* mask, uint64_t cand) {
     }
 }
 
-/* Transforms on caller-given uniforms: B1/B2/P/P2/R use 2 per pair, B3 3 per pair.
+/* Transforms on caller-given uniforms: B1/B2/P/P2/R/R1 use 2 per pair, B3 3 per pair.
  * method: 1,2,3 = B1,B2,B3; 4 = P, 5 = P2 (rejected candidates give NaN, NaN and mask 0);
- * 6 = R: out[2j] = sigma x + mu (NaN if rejected), out[2j+1] = x (always). */
+ * 6 = R: out[2j] = sigma x + mu (NaN if rejected), out[2j+1] = x (always);
+ * 7 = R1: as 6, and mask = accept | (step-2.5 class << 1). */
 int orc_transform_from_uniforms(const double* u, uint64_t n_pairs, double* out, uint8_t* mask, double mu,
                                 double sigma, int method) {
-    if (method < 1 || method > 6) return -1;
+    if (method < 1 || method > 7) return -1;
 #pragma omp parallel for schedule(static)
     for (long j = 0; j < (long)n_pairs; ++j) {
         double x = NAN, y = NAN;
@@ -453,6 +512,13 @@ int orc_transform_from_uniforms(const double* u, uint64_t n_pairs, double* out, 
             double ab[2];
             int acc = ratio_candidate(u[2 * j], u[2 * j + 1], &y, ab);
             if (mask) mask[j] = (uint8_t)acc;
+            if (acc) x = fma(sigma, y, mu);
+        }
+        else if (method == 7) {
+            double a;
+            int cls = ratio1_pretest(u[2 * j], u[2 * j + 1], &y, &a);
+            int acc = cls == 1 || (cls == 0 && !(a > -4.0 * log(1.0 - u[2 * j])));
+            if (mask) mask[j] = (uint8_t)(acc | (cls << 1));
             if (acc) x = fma(sigma, y, mu);
         } else {
             double cx, cy, s;
