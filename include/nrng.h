@@ -109,6 +109,14 @@ int nrng_normal_polar2(nrng_handle h, double* out, size_t n, double mu, double s
  * Errors as nrng_normal_polar.  Not available in the sequential mode. */
 int nrng_normal_ratio(nrng_handle h, double* out, size_t n, double mu, double sigma);
 
+/* Algorithm R1: Algorithm R with step 2.5, the pretests P1
+ * (accept without a logarithm) and P2 (reject) before step 3 -- reading R29: the tangent-line
+ * bounds of ln with a 2^-40 safety margin, so they never decide differently from step 3.
+ * Same arguments, layout, exact stop, output and uniform consumption as nrng_normal_ratio
+ * (identical results); only ~17% of the candidates (the borderline region) evaluate the
+ * logarithm, gathered into one pass per warp step.  Errors as nrng_normal_polar. */
+int nrng_normal_ratio1(nrng_handle h, double* out, size_t n, double mu, double sigma);
+
 /* ---- sequential mode: RANN3-style buffering ----
  * One canonical, partition-invariant sequence per handle and method: epoch e is the output
  * of every stream making E more pairs, stream-major (2 S E deviates; E = epoch_pairs, a
@@ -155,7 +163,9 @@ int nrng_polar_mask(nrng_handle h, uint8_t* dev_mask, size_t cand_per_stream);
 /* Transforms on caller-given device uniforms (no generator state involved):
  * method 1/2/3 = B1/B2/B3 (2/2/3 uniforms per pair), 4 = Polar candidate, 5 = P2 candidate
  * (2 uniforms; rejected -> NaN outputs and dev_mask 0; dev_mask may be NULL), 6 = R
- * candidate (2 uniforms: out[2j] = sigma x + mu, NaN if rejected; out[2j+1] = x).
+ * candidate (2 uniforms: out[2j] = sigma x + mu, NaN if rejected; out[2j+1] = x), 7 = R1
+ * candidate (as 6; dev_mask = accepted | step-2.5 class << 1, class 1 = P1, 2 = P2,
+ * 0 = borderline).
  * out: 2*n_pairs.
  * Enqueued on cuda_stream. */
 int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* dev_out, uint8_t* dev_mask,

@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("NRNG_LIB_OVERRIDE") or os.path.join(PKG, "libnrng.so"
 NRNG_DEFAULT, NRNG_B1, NRNG_B2, NRNG_B3, NRNG_POLAR, NRNG_POLAR2 = 0, 1, 2, 3, 4, 5
 NRNG_OK, NRNG_EINVAL, NRNG_ENOMEM, NRNG_ECUDA, NRNG_ENODEV = 0, -1, -2, -3, -4
 LAG_R = 607
-METHODS = {"B1": 1, "B2": 2, "B3": 3, "P": 4, "P2": 5, "R": 6}
+METHODS = {"B1": 1, "B2": 2, "B3": 3, "P": 4, "P2": 5, "R": 6, "R1": 7}
 
 # name -> (argtypes, restype); mirrors include/nrng.h one to one
 _u64, _u32, _dbl, _p, _int, _sz = C.c_uint64, C.c_uint32, C.c_double, C.c_void_p, C.c_int, C.c_size_t
@@ -34,6 +34,7 @@ SIGNATURES = {
     "nrng_normal_polar": ([_p, _p, _sz, _dbl, _dbl], _int),
     "nrng_normal_polar2": ([_p, _p, _sz, _dbl, _dbl], _int),
     "nrng_normal_ratio": ([_p, _p, _sz, _dbl, _dbl], _int),
+    "nrng_normal_ratio1": ([_p, _p, _sz, _dbl, _dbl], _int),
     "nrng_serial_corr": ([_p, _sz, _dbl, _int, _p, _p], _int),
     "nrng_serial_corr_blocks": ([_sz], _sz),
     "nrng_seq_configure": ([_p, _u32], _int),
@@ -130,6 +131,10 @@ def nrng_normal_polar2(h, out_ptr: int, n: int, mu: float, sigma: float) -> None
 
 def nrng_normal_ratio(h, out_ptr: int, n: int, mu: float, sigma: float) -> None:
     _check(lib().nrng_normal_ratio(h, out_ptr, n, mu, sigma), "nrng_normal_ratio")
+
+
+def nrng_normal_ratio1(h, out_ptr: int, n: int, mu: float, sigma: float) -> None:
+    _check(lib().nrng_normal_ratio1(h, out_ptr, n, mu, sigma), "nrng_normal_ratio1")
 
 
 def nrng_seq_configure(h, epoch_pairs: int) -> None:
@@ -295,6 +300,13 @@ class Generator:
         nrng_normal_ratio(self.h, ptr, n, mu, sigma)
         return out
 
+    def normal_ratio1(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
+        """Algorithm R1 (R with the step-2.5 pretests): the same output as normal_ratio."""
+        out, ptr, n = self._out(n, out)
+        self._sync_stream()
+        nrng_normal_ratio1(self.h, ptr, n, mu, sigma)
+        return out
+
     def normal(self, method: str, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
         if method == "P":
             return self.normal_polar(n, mu, sigma, out=out)
@@ -302,6 +314,8 @@ class Generator:
             return self.normal_polar2(n, mu, sigma, out=out)
         if method == "R":
             return self.normal_ratio(n, mu, sigma, out=out)
+        if method == "R1":
+            return self.normal_ratio1(n, mu, sigma, out=out)
         return self.normal_boxmuller(n, mu, sigma, METHODS[method], out=out)
 
     def normal_seq(self, method: str, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
@@ -342,7 +356,8 @@ class Generator:
 
 
 def transform_from_uniforms(u, method: int, mu: float = 0.0, sigma: float = 1.0):
-    """Device transform on given uniforms: method 1/2/3 = B1/B2/B3, 4 = Polar, 5 = P2, 6 = R.  Returns (out, mask)."""
+    """Device transform on given uniforms: method 1/2/3 = B1/B2/B3, 4 = Polar, 5 = P2, 6 = R, 7 = R1.
+    Returns (out, mask)."""
     torch = _torch()
     per = 3 if method == 3 else 2
     n_pairs = u.numel() // per

@@ -34,13 +34,14 @@ int cuda_err(cudaError_t e) {
 }
 
 constexpr size_t bm_smem(int nw) { return win_bytes(nw) + kTabBytes; }
+constexpr size_t r1_smem(int nw) { return bm_smem(nw) + (size_t)nw * 32 * sizeof(double); }  // + R1 scratch
 constexpr size_t polar_smem(int nw) { return win_bytes(nw) + kTabBytes; }
 constexpr size_t kUniSmem = win_bytes(kWarpsPerBlock);
 constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
 constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)
 
 struct Occ {
-    int bm[4] = {0, 0, 0, 0}, polar = 0, ratio = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
+    int bm[4] = {0, 0, 0, 0}, polar = 0, ratio = 0, ratio1 = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
 };
 
 }  // namespace
@@ -96,7 +97,7 @@ unsigned grid_for(uint32_t nstreams, int nw, int per_sm, int num_sms) {
 // Launch one bulk kernel over streams [b, e) of the handle.  Stream counts that fill every
 // SM with kBigBlock-warp blocks use those (one block per SM); smaller ones use 4-warp
 // blocks spread over all SMs.
-enum class Kind { BM1, BM2, BM3, POLAR, POLAR2, RATIO, UNIFORM };
+enum class Kind { BM1, BM2, BM3, POLAR, POLAR2, RATIO, RATIO1, UNIFORM };
 
 template <int V>
 void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
@@ -144,7 +145,8 @@ cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st)
             case Kind::BM2: tiny_kernel<2><<<grid, kTinyThreads, 0, st>>>(p); break;
             case Kind::BM3: tiny_kernel<3><<<grid, kTinyThreads, 0, st>>>(p); break;
             case Kind::POLAR2: tiny_kernel<5><<<grid, kTinyThreads, 0, st>>>(p); break;
-            case Kind::RATIO: tiny_kernel<6><<<grid, kTinyThreads, 0, st>>>(p); break;
+            case Kind::RATIO:   // R1's pretests change no output: its short calls are R's
+            case Kind::RATIO1: tiny_kernel<6><<<grid, kTinyThreads, 0, st>>>(p); break;
             default: tiny_kernel<4><<<grid, kTinyThreads, 0, st>>>(p); break;
         }
         h->launches += 1;
@@ -162,6 +164,13 @@ cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st)
             else
                 pw_kernel<6, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.ratio, h->num_sms),
                                                 kWarpsPerBlock * 32, bm_smem(kWarpsPerBlock), st>>>(p);
+            break;
+        case Kind::RATIO1:
+            if (ns >= (uint32_t)(kPwWarps * h->num_sms))
+                pw_kernel<7, kPwWarps><<<h->num_sms, kPwWarps * 32, r1_smem(kPwWarps), st>>>(p);
+            else
+                pw_kernel<7, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.ratio1, h->num_sms),
+                                                kWarpsPerBlock * 32, r1_smem(kWarpsPerBlock), st>>>(p);
             break;
         case Kind::UNIFORM:
             uniform_kernel<<<grid_for(ns, kWarpsPerBlock, h->occ.uni, h->num_sms), kWarpsPerBlock * 32, kUniSmem,
@@ -289,6 +298,8 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(pw_kernel<5, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
     occupancy(pw_kernel<6, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
     h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    occupancy(pw_kernel<7, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
+    h->occ.ratio1 = occupancy(pw_kernel<7, kWarpsPerBlock>, kWarpsPerBlock, r1_smem(kWarpsPerBlock));
     occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     occupancy(polar_kernel<kBigBlockPolar, 2>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     h->occ.uni = occupancy(uniform_kernel, kWarpsPerBlock, kUniSmem);
@@ -383,6 +394,13 @@ int nrng_normal_ratio(nrng_handle h, double* out, size_t n, double mu, double si
     if (!check_device(h)) return set_err(NRNG_EINVAL);
     if (n == 0) return set_err(NRNG_OK);
     return run_bulk(h, Kind::RATIO, out, n, n, 1, mu, sigma);  // units: normals (R26)
+}
+
+int nrng_normal_ratio1(nrng_handle h, double* out, size_t n, double mu, double sigma) {
+    if (!h || (n > 0 && !out) || bad_params(mu, sigma)) return set_err(NRNG_EINVAL);
+    if (!check_device(h)) return set_err(NRNG_EINVAL);
+    if (n == 0) return set_err(NRNG_OK);
+    return run_bulk(h, Kind::RATIO1, out, n, n, 1, mu, sigma);  // units: normals (R26)
 }
 
 // ---------------------------------------------------------------- sequential mode
@@ -505,7 +523,7 @@ int nrng_polar_mask(nrng_handle h, uint8_t* dev_mask, size_t cand_per_stream) {
 
 int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* dev_out, uint8_t* dev_mask, double mu,
                                  double sigma, int method, void* cuda_stream) {
-    if ((n_pairs > 0 && (!dev_u || !dev_out)) || bad_params(mu, sigma) || method < 1 || method > 6)
+    if ((n_pairs > 0 && (!dev_u || !dev_out)) || bad_params(mu, sigma) || method < 1 || method > 7)
         return set_err(NRNG_EINVAL);
     if (n_pairs == 0) return set_err(NRNG_OK);
     int dev = 0, sms = 148;

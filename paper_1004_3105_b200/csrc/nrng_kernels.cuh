@@ -639,7 +639,8 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
 // the end).  Word i of the call (i < 0: the loaded state) is at logical position i mod 1024.
 // Used for aligned, plain-layout calls filling the GPU; the rest go to bm_kernel /
 // polar_kernel.  M: 1 = B1, 2 = B2, 4 = P (P2 keeps polar_kernel: here it spilled), 6 = R
-// (Algorithm R, the only path for it besides the tiny-quota kernel).
+// (Algorithm R, the only path for it besides the tiny-quota kernel), 7 = R1 (R with the
+// step-2.5 pretests; needs 32 more doubles of shared scratch per warp, pw_smem).
 #ifndef NRNG_PW_WARPS
 #define NRNG_PW_WARPS 16  // measured (ms per 2^31, B1/B2/P): 16 warps 3.68/3.88/4.52, 12: 4.09/3.83/4.54, 14: 4.28/4.21/4.72, 18: 4.06/4.44/4.73, 20 (another box): 3.79/4.19/4.30
 #endif
@@ -846,6 +847,31 @@ __device__ __forceinline__ bool pw_ratio_block(const PwPtrs& pp, const TParams& 
     return stop;
 }
 
+// One Algorithm R1 step (128 candidates) at compile-time base K: R's step with the step-2.5
+// pretests and the borderline logarithms gathered (ratio1_decide); the same output.
+template <int K>
+__device__ __forceinline__ bool pw_ratio1_block(const PwPtrs& pp, const TParams& tp, const Tables& tab, double* o,
+                                                double* scr, uint32_t cnt, uint32_t& acc, uint32_t& used, int lane,
+                                                unsigned lt) {
+    uint64_t wa[kPU], wb[kPU];
+    pw_gen_c<kPU, K>(pp, wa, wb);
+    double Nu[kPU], x[kPU], a[kPU];
+    int cls[kPU];
+    ratio1_pretest<kPU>(wa, wb, Nu, x, a, cls);
+    bool ok[kPU];
+    ratio1_decide<kPU>(Nu, a, cls, tab, scr, lane, lt, ok);
+    unsigned m[kPU];
+    bool stop;
+    used = polar_rank(ok, m, cnt - acc, lt, stop);
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) {
+        if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), __fma_rn(tp.sigma, x[u], tp.mu));
+        acc += __popc(m[u]);
+    }
+    __syncwarp();
+    return stop;
+}
+
 template <int M, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
@@ -856,6 +882,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     const PwLane ol = pw_lane(lane);
     const PwPtrs pp = pw_ptrs(buf, ol);
     const unsigned lt = lanemask_lt(lane);
+    double* const scr = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + 32 * warp;  // M = 7 only
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
@@ -922,6 +949,22 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
                 K = (K + 64) & kWinMask;
             }
             used = 2 * qk.cnt;
+        } else if constexpr (M == 7) {
+            // Algorithm R1: R with the step-2.5 pretests (reading R29); the same output.
+            double* const o = p.out + (qk.off - p.shift);
+            const uint32_t cnt = (uint32_t)qk.cnt;
+            uint32_t acc = 0, blocks = 0, usedc = 0;
+            for (;;) {
+                if (pw_ratio1_block<0>(pp, p.tp, tab, o, scr, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_ratio1_block<256>(pp, p.tp, tab, o, scr, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_ratio1_block<512>(pp, p.tp, tab, o, scr, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+                if (pw_ratio1_block<768>(pp, p.tp, tab, o, scr, cnt, acc, usedc, lane, lt)) break;
+                ++blocks;
+            }
+            used = (uint64_t)kBlk * blocks + 2 * usedc;
         } else if constexpr (M == 6) {
             // Algorithm R: 128 candidates per step, one normal per accepted candidate (R26).
             double* const o = p.out + (qk.off - p.shift);
@@ -1192,6 +1235,20 @@ __global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs,
         } else if (method == 3) {
             const uint64_t w1[1] = {word_of(u[3 * j])}, w2[1] = {word_of(u[3 * j + 1])}, w3[1] = {word_of(u[3 * j + 2])};
             b3_pairs<1>(w1, w2, w3, tp, tab, x, y);
+        } else if (method == 7) {
+            const uint64_t wu[1] = {word_of(u[2 * j])}, wv[1] = {word_of(u[2 * j + 1])};
+            double Nu[1], xr[1], a[1];
+            int cls[1];
+            ratio1_pretest<1>(wu, wv, Nu, xr, a, cls);
+            bool ok = cls[0] == 1;
+            if (cls[0] == 0) {  // step 3 (the kernel path gathers these; here one per thread)
+                double L[1];
+                fast_log<1>(Nu, -53, tab, L);
+                ok = !(a[0] > __dmul_rn(-4.0, L[0]));
+            }
+            if (mask) mask[j] = (uint8_t)((ok ? 1 : 0) | (cls[0] << 1));
+            if (ok) x[0] = __fma_rn(tp.sigma, xr[0], tp.mu);
+            y[0] = xr[0];
         } else if (method == 6) {
             const uint64_t wu[1] = {word_of(u[2 * j])}, wv[1] = {word_of(u[2 * j + 1])};
             double xr[1];

@@ -294,6 +294,64 @@ def test_ratio_bench_shape_sampled_and_host_output():
     assert np.array_equal(h, gen_normals(g2, "R", h.size, 0.5, 3.0))
 
 
+# ---------------------------------------------------------------- Algorithm R1 (R + step 2.5)
+
+def test_ratio1_transform_from_uniforms():
+    u = W.dyadic_uniforms(107, 2 * 400001)
+    e = W.edge_uniforms()
+    u = np.concatenate([np.array([[a, b] for a in e for b in e]).ravel(), u])
+    mu, sigma = 0.25, 2.0
+    d_out, d_mask = P.transform_from_uniforms(torch.from_numpy(u).cuda(), 7, mu, sigma)
+    o_out, o_mask = O.transform_from_uniforms(u, 7, mu, sigma)
+    r_out, r_mask = O.transform_from_uniforms(u, 6, mu, sigma)
+    d_out, d_mask = host(d_out), host(d_mask)
+    # step 2.5 classes: P1 / P2 / borderline, as the oracle classifies them; each pretest
+    # agrees with step 3 (R's oracle decision), and all three classes occur
+    assert np.array_equal(d_mask >> 1, o_mask >> 1)
+    cls, acc_r = d_mask >> 1, r_mask.astype(bool)
+    assert np.all(acc_r[cls == 1]) and not np.any(acc_r[cls == 2])
+    assert 0.12 < (cls == 0).mean() < 0.22 and (cls == 1).mean() > 0.6
+    # x bit-exact; decisions and outputs equal R's wherever ln's last bits cannot matter (R27)
+    assert np.array_equal(d_out[1::2], r_out[1::2])
+    safe = _ratio_margin(u[0::2], u[1::2]) > 1e-12
+    assert np.array_equal((d_mask & 1)[safe], r_mask[safe])
+    acc = acc_r & safe
+    assert np.array_equal(d_out[0::2][acc], r_out[0::2][acc])
+    assert np.all(np.isnan(d_out[0::2][~(d_mask & 1).astype(bool)]))
+
+
+@pytest.mark.parametrize("S,ns", [(64, [1, 3, 2 * 64 + 1, 64 * 33 + 5, 64 * 700 + 17]),
+                                  (1000, [1000 * 130 + 999, 7]),
+                                  (4160, [4160 * 40 + 2345, 4160 * 3 + 7, 4160 * 129])])
+def test_ratio1_bulk_parity(S, ns):
+    # R1 returns exactly Algorithm R's output (reading R29): against the oracle's R and R1,
+    # tiny, 4-warp and one-block-per-SM kernels, consecutive calls, state bit-exact
+    g, st, st1 = P.Generator(21, S, first_stream=5), O.Streams(21, S, first_stream=5), O.Streams(21, S, first_stream=5)
+    for n in ns:
+        d = gen_normals(g, "R1", n, -1.0, 2.0)
+        o = ora_normals(st, "R", n, -1.0, 2.0)
+        assert st.ratio_margin > 1e-12
+        assert d.size == n and np.array_equal(d, o), (S, n)
+        assert np.array_equal(st1.normal_ratio1(n, -1.0, 2.0), o)
+    assert_state_equal(g, st)
+
+
+def test_ratio1_bench_shape_sampled():
+    c = W.C5_SHARD
+    g = P.Generator(c.seed, c.streams)
+    out = torch.empty(c.n, dtype=torch.float64, device="cuda")
+    g.normal("R1", out=out)
+    per = c.n // c.streams
+    counts = g.stream_counts()
+    for k in [0, 1, 4242, c.streams - 1]:
+        st = O.Streams(c.seed, 1, first_stream=k)
+        o = st.normal_ratio(per)
+        assert st.ratio_margin > 1e-12
+        assert np.array_equal(host(out[k * per:(k + 1) * per]), o)
+        assert counts[k] == st.counts[0]
+    del out
+
+
 # ---------------------------------------------------------------- serial correlation gate
 
 def test_serial_corr_kernel_matches_numpy():

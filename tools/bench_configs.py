@@ -61,7 +61,7 @@ def main():
     big = torch.empty(1 << 31, dtype=torch.float64, device="cuda")
     for c in (W.C1, W.C2, W.C3):
         g = P.Generator(c.seed, c.streams)
-        for m in c.methods + (("P2", "R") if c.name == "C2" else ()):
+        for m in c.methods + (("P2", "R", "R1") if c.name == "C2" else ()):
             res["%s_%s" % (c.name, m)] = time_calls(g, m, c.n, c.mu, c.sigma, big, args.calls)
         g.close()
     c = W.C4
@@ -77,7 +77,7 @@ def main():
     g.close()
     c = W.C5_SHARD
     g = P.Generator(c.seed, c.streams)
-    for m in c.methods + ("P2", "R"):
+    for m in c.methods + ("P2", "R", "R1"):
         res["C5shard_%s" % m] = time_calls(g, m, c.n, c.mu, c.sigma, big, 5)
     print(json.dumps(res, indent=1))
 

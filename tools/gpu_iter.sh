@@ -10,5 +10,5 @@ d = json.loads(open("gpurun_out/bench_$TAG.log").read().strip().splitlines()[-1]
 print("value %.4g" % d["value"], {m: ("%.3g/s" % v["normals_per_s"], "%.3f ms" % v["ms_per_call"]) for m, v in d["per_method"].items()}, d["clocks"])
 PY
 if [ "${NCU:-1}" = "1" ]; then
-python tools/profile_step.py > gpurun_out/plain_$TAG.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"pw_kernel|b3_kernel|polar" -s 6 -c 6 -o gpurun_out/prof_$TAG python tools/profile_step.py > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu rc=$?"
+python tools/profile_step.py > gpurun_out/plain_$TAG.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"pw_kernel|b3_kernel|polar" -s 7 -c 7 -o gpurun_out/prof_$TAG python tools/profile_step.py > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu rc=$?"
 fi

@@ -14,7 +14,7 @@ import paper_1004_3105_b200 as P  # noqa: E402
 from paper_1004_3105_b200 import workloads as W  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--methods", default="B1,B2,B3,P,P2,R")
+ap.add_argument("--methods", default="B1,B2,B3,P,P2,R,R1")
 ap.add_argument("--log2n", type=int, default=31)
 args = ap.parse_args()
 c = W.C5_SHARD
