@@ -265,7 +265,8 @@ constexpr int kTriMirror = 2 * kTriRow;
 constexpr int kTriAlloc = kTriWin + kTriMirror;
 constexpr int kTriScratch = 32;  // per-warp tail-compaction slots (doubles)
 #ifndef NRNG_TRI_WARPS
-#define NRNG_TRI_WARPS 16  // measured: 16 warps (107 registers, no rematerialisation) 5.79 ms, 20 warps (96) 5.94, 12 warps 5.82
+#define NRNG_TRI_WARPS 16  // measured (11-row window): 16 warps 5.79 ms, 20 warps 5.94, 12 warps 5.82; 12-row window:
+                           // 12 warps 5.89-5.96 vs 16 warps 5.80-5.84 (sustained); 20 warps no longer fit in 227 KB
 #endif
 constexpr int kTriWarps = NRNG_TRI_WARPS;
 static_assert(kTriWin >= kLagR + 4 * kTriRow && 2 * kTriRow < kLagS && kTriWin % (4 * kTriRow) == 0,
