@@ -35,7 +35,7 @@ int cuda_err(cudaError_t e) {
 
 constexpr size_t bm_smem(int nw) { return win_bytes(nw) + kTabBytes; }
 constexpr size_t r1_smem(int nw) { return bm_smem(nw) + (size_t)nw * 32 * sizeof(double); }  // + R1 scratch
-constexpr size_t polar_smem(int nw) { return win_bytes(nw) + kTabBytes; }
+constexpr size_t polar_smem(int nw) { return win_bytes(nw) + kTabBytes + (size_t)nw * 32 * sizeof(double); }  // + P2 tail scratch
 constexpr size_t kMaxSmem = 227 * 1024;  // per block, sm_100a opt-in maximum
 static_assert(bm_smem(kPwWarps) <= kMaxSmem && r1_smem(kPwWarps) <= kMaxSmem && tri_smem(kTriWarps) <= kMaxSmem &&
                   bm_smem(kBigBlock) <= kMaxSmem && polar_smem(kBigBlockPolar) <= kMaxSmem,

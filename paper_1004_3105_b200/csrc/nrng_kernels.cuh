@@ -509,6 +509,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
     const unsigned lt = lanemask_lt(lane);
+    double* const scr = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + 32 * warp;  // P2 tails
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
@@ -550,7 +551,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 if (!stop) phase_gen_store(bl, nb, g);
                 double ox[kPU], oy[kPU];
                 if (M == 2)
-                    p2_transform<kPU>(c, p.tp, tab, ox, oy);
+                    p2_transform_compact<kPU>(c, ok, p.tp, tab, scr, lane, lt, ox, oy);
                 else
                     polar_transform<kPU>(c, p.tp, tab, ox, oy);
 #pragma unroll
@@ -586,7 +587,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 const uint32_t used = polar_rank(ok, m, cnt - acc, lt, stop);
                 double ox[kPU], oy[kPU];
                 if (M == 2)
-                    p2_transform<kPU>(c, p.tp, tab, ox, oy);
+                    p2_transform_compact<kPU>(c, ok, p.tp, tab, scr, lane, lt, ox, oy);
                 else
                     polar_transform<kPU>(c, p.tp, tab, ox, oy);
                 uint32_t j = acc;
