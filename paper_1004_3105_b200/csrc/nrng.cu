@@ -124,7 +124,7 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
                                        bm_smem(kWarpsPerBlock), st>>>(p);
 }
 
-#ifndef NRNG_P2_PW  // P2 on pw_kernel<5>: 128 registers + 20 B spills at 16 warps, 7.05 ms vs 6.34 (polar_kernel)
+#ifndef NRNG_P2_PW  // P2 on pw_kernel<5> (compacted tails, 104 registers): 6.25 ms vs 6.21 on polar_kernel
 #define NRNG_P2_PW 0
 #endif
 template <int M>
@@ -132,7 +132,7 @@ void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t 
     constexpr int kPw = M == 1 ? 4 : 5;  // pw_kernel's P and P2 transforms
     if ((M == 1 || NRNG_P2_PW) && p.aligned && p.log2E == 0 && p.q + 1 < (1ull << 31) &&
         ns >= (uint32_t)(kPwWarps * h->num_sms))
-        pw_kernel<kPw, kPwWarps><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
+        pw_kernel<kPw, kPwWarps><<<h->num_sms, kPwWarps * 32, kPw == 5 ? r1_smem(kPwWarps) : bm_smem(kPwWarps), st>>>(p);
     else if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
         polar_kernel<kBigBlockPolar, M><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
     else
@@ -299,7 +299,7 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(pw_kernel<1, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
     occupancy(pw_kernel<2, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
     occupancy(pw_kernel<4, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
-    occupancy(pw_kernel<5, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(pw_kernel<5, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
     occupancy(pw_kernel<6, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
     h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     occupancy(pw_kernel<7, kPwWarps>, kPwWarps, r1_smem(kPwWarps));

@@ -793,7 +793,8 @@ __device__ __forceinline__ void pw_bm_block(const PwPtrs& pp, const TParams& tp,
 template <int M, int K>
 __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& tp, const Tables& tab,
                                                const BulkParams& p, const Quota& qk, double2* o, bool direct,
-                                               uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt) {
+                                               uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt,
+                                               double* scr) {
     uint64_t wa[kPU], wb[kPU];
     pw_gen_c<kPU, K>(pp, wa, wb);
     PolarCand c[kPU];
@@ -804,8 +805,8 @@ __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& 
     bool stop;
     used = polar_rank(ok, m, cnt - acc, lt, stop);
     double ox[kPU], oy[kPU];
-    if (M == 5)
-        p2_transform<kPU>(c, tp, tab, ox, oy);
+    if constexpr (M == 5)
+        p2_transform_compact<kPU>(c, ok, tp, tab, scr, lane, lt, ox, oy);
     else
         polar_transform<kPU>(c, tp, tab, ox, oy);
     if (direct) {
@@ -884,7 +885,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     const PwLane ol = pw_lane(lane);
     const PwPtrs pp = pw_ptrs(buf, ol);
     const unsigned lt = lanemask_lt(lane);
-    double* const scr = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + 32 * warp;  // M = 7 only
+    double* const scr = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + 32 * warp;  // M = 5, 7
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
@@ -990,13 +991,13 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
             const uint32_t cnt = (uint32_t)qk.cnt;
             uint32_t acc = 0, blocks = 0, usedc = 0;
             for (;;) {
-                if (pw_polar_block<M, 0>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt)) break;
+                if (pw_polar_block<M, 0>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr)) break;
                 ++blocks;
-                if (pw_polar_block<M, 256>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt)) break;
+                if (pw_polar_block<M, 256>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr)) break;
                 ++blocks;
-                if (pw_polar_block<M, 512>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt)) break;
+                if (pw_polar_block<M, 512>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr)) break;
                 ++blocks;
-                if (pw_polar_block<M, 768>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt)) break;
+                if (pw_polar_block<M, 768>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr)) break;
                 ++blocks;
             }
             used = (uint64_t)kBlk * blocks + 2 * usedc;
