@@ -354,7 +354,7 @@ def main():
         # calibrate on 256 streams, then size the sample for ~10 s of oracle wall time
         cv, _, _, csecs = oracle_sample(256, threads)
         ns = int(min(CFG.streams, max(256, 256 * 10.0 / max(csecs, 1e-3))))
-        ns = 1 << int(math.log2(ns))
+        ns = min(CFG.streams, 1 << int(round(math.log2(ns))))
         cv, cper, cn, csecs = oracle_sample(ns, threads)
         cpu = {"value": cv, "unit": "normals/s", "cores": threads, "kind": "oracle",
                "sample": "%d streams x 2^14 pairs per method (B1,B2,B3,P) = %d normals per method, %.1f s wall"
