@@ -47,6 +47,25 @@ constexpr int kBigBlockPolar = 20;
 // ------------------------------------------------------------------ seeding + warm-up
 // Word j of global stream g = splitmix64 output #(607 g + j) of seed (R2); all-even fix
 // (R4); 10 rounds of the round update (3 dependency phases 273/273/61) discarded (R3).
+// L2 prefetch of the state of stream kn (its 4864-byte ring row = 38 lines, and its counter),
+// issued when a warp starts a stream, for the stream it will take next: that stream's state
+// load then hits L2 instead of paying an HBM round trip at the head of its serial chain (the
+// mid-size configs run only a few blocks per stream, so that latency is not hidden).
+#ifndef NRNG_PREFETCH_STATE  // 0: off, 1: when the warp starts a stream, 2: after its state load
+#define NRNG_PREFETCH_STATE 2  // measured (us per call, off -> 2): C3 B2 603 -> 536, B3 806 -> 723, C4 B1 n=2^26
+#endif                         // 278 -> 214, C1 11.3 -> 11.3, C2 P 70.5 -> 72.2; bench shape within +-2%
+#ifndef NRNG_PREFETCH_B1
+#define NRNG_PREFETCH_B1 1
+#endif
+template <int MODE>
+__device__ __forceinline__ void prefetch_state(const BulkParams& p, uint32_t kn, int lane) {
+    if (NRNG_PREFETCH_STATE != MODE || kn >= p.s_end) return;
+    static_assert(kPitch * 8 == 38 * 128, "ring row = 38 lines");
+    const char* row = reinterpret_cast<const char*>(p.ring + (uint64_t)kn * kPitch);
+    for (int l = lane; l < 38; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 128 * l));
+    if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.count + kn));
+}
+
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) init_kernel(uint64_t* __restrict__ ring,
                                                                    uint64_t* __restrict__ count, uint64_t seed,
                                                                    uint64_t first_stream, uint32_t S) {
@@ -136,9 +155,11 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
+        prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         lfg_load(L, rk, C, lane, qk.cnt * per < (uint64_t)kLagR ? (uint32_t)(qk.cnt * per) : (uint32_t)kLagR);
+        prefetch_state<2>(p, k + gridDim.x * NW, lane);
         uint64_t j0 = 0;
         if (p.aligned && 2 * (qk.off + qk.cnt) <= p.n) {
             double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
@@ -383,6 +404,7 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
+        prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         {   // x_{C-607+j} -> position 1152 - 607 + j
@@ -394,6 +416,7 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
             }
         }
         __syncwarp();
+        prefetch_state<2>(p, k + gridDim.x * NW, lane);
         // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
         const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
         const uint32_t nit = (uint32_t)(safe_cnt / 128);  // full 4-row iterations (a 32-bit count: no
@@ -513,9 +536,11 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
+        prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         lfg_load(L, rk, C, lane);
+        prefetch_state<2>(p, k + gridDim.x * NW, lane);
         const bool fast = p.aligned && 2 * (qk.off + qk.cnt) <= p.n;
         const bool direct = fast && p.log2E == 0;
         const bool phased = direct && qk.cnt < (1ull << 31);
@@ -889,6 +914,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p.q, p.rem, k);
         if (qk.cnt == 0) continue;
+        if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         {   // x_{C-607+j} -> logical position 417 + j
@@ -900,6 +926,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
             }
         }
         __syncwarp();
+        if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<2>(p, k + gridDim.x * NW, lane);
         uint64_t used;  // words consumed by this call
         if constexpr (M <= 2) {
             // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
