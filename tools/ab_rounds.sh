@@ -1,6 +1,7 @@
 #!/bin/bash
-# Interleaved A/B: ROUNDS x (each lib in its own process), best-of-3 per method, with the SM
-# clock sampled during each run.  usage: bash tools/ab_rounds.sh ROUNDS METHODS LIB1 LIB2 ...
+# Interleaved A/B: ROUNDS x (each lib in its own process), best-of-3 per method after AB_WARM
+# (default 25) warm-up calls of that method (the board's power controller carries state from one
+# kernel to the next), with the SM clock sampled during each run.  usage: bash tools/ab_rounds.sh ROUNDS METHODS LIB1 LIB2 ...
 ROUNDS=$1; METHODS=$2; shift 2
 for r in $(seq $ROUNDS); do
   for lib in "$@"; do
@@ -15,7 +16,7 @@ from paper_1004_3105_b200 import workloads as W
 c=W.C5_SHARD; g=P.Generator(c.seed,c.streams); out=torch.empty(c.n,dtype=torch.float64,device='cuda')
 res=[]
 for m in "$METHODS".split(','):
-    for _ in range(2): g.normal(m,out=out)
+    for _ in range(int('${AB_WARM:-25}')): g.normal(m,out=out)  # settle the power controller on this method
     torch.cuda.synchronize(); a=torch.cuda.Event(enable_timing=True); b=torch.cuda.Event(enable_timing=True)
     best=1e9
     for rep in range(3):
