@@ -1388,41 +1388,62 @@ __global__ void gof_hist_kernel(const double* __restrict__ x, uint64_t n, double
 }
 
 // ------------------------------------------------------------------ serial correlation
-// Lagged products for the serial-correlation gate: tile t
-// covers x[t T, t T + T + K) (minus `center`), staged in shared memory; thread k < K+1 sums
-// d_i d_{i+k} over the tile's i with i + k < n.  Blocks stride over the tiles (a fixed grid
-// of min(#tiles, kCorrGrid) blocks, independent of the device, so the summation order is
-// deterministic) and write partial[b][k]; the host sums the blocks in order.  The shared
-// reads are a broadcast (d_i) and a contiguous run (d_{i+k}).  Validation only.
+// Lagged products for the serial-correlation gate:
+// S_k = sum_i d_i d_{i+k}, d_i = x_i - center, k = 0..127 (K <= 127 are written).  Tile t
+// covers x[t T, t T + T + 136) staged in shared memory (zero past n); blocks stride over the
+// tiles (a fixed grid of min(#tiles, kCorrGrid) blocks, independent of the device, so the
+// summation order is deterministic) and write partial[b][k]; the host sums the blocks.
+// Register blocking: thread (half h, i-phase r = 0..7, lag phase g = 0..7) owns the 16 lags
+// k = g + 8 j and the i = r (mod 8) of its half-tile, keeping the 16 values d_{i+g+8j} in a
+// register ring: each step (i += 8) is one broadcast load of d_i, one load of the new
+// d_{i+g+128} and 16 FMAs -- FP64-bound instead of two shared loads per FMA.
 constexpr int kCorrTile = 4096;
 constexpr int kCorrMaxLag = 127;
+constexpr int kCorrPad = 136;  // 128 lags + one 8-step stride of lookahead
 constexpr unsigned kCorrGrid = 2048;
 __global__ void __launch_bounds__(128) serial_corr_kernel(const double* __restrict__ x, uint64_t n, double center,
                                                           int K, double* __restrict__ partial) {
-    __shared__ double d[kCorrTile + kCorrMaxLag];
-    const int k = threadIdx.x;
+    __shared__ double d[kCorrTile + kCorrPad];
+    static_assert(16 * 129 <= kCorrTile + kCorrPad, "the reduction reuses the tile");
+    const int t = threadIdx.x, h = t >> 6, r = t & 7, g = (t >> 3) & 7;
     const uint64_t tiles = (n + kCorrTile - 1) / kCorrTile;
-    double s0 = 0.0, s1 = 0.0;
-    for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const uint64_t base = t * kCorrTile;
+    double acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+    for (uint64_t tt = blockIdx.x; tt < tiles; tt += gridDim.x) {
+        const uint64_t base = tt * kCorrTile;
         __syncthreads();
-        for (int j = threadIdx.x; j < kCorrTile + K; j += blockDim.x) {
+        for (int j = t; j < kCorrTile + kCorrPad; j += blockDim.x) {
             const uint64_t i = base + j;
             d[j] = i < n ? x[i] - center : 0.0;  // zero padding past n contributes nothing
         }
         __syncthreads();
-        if (k <= K) {
-            const uint64_t left = n - base;
-            const int T = left < (uint64_t)kCorrTile ? (int)left : kCorrTile;
-            int i = 0;
-            for (; i + 1 < T; i += 2) {
-                s0 = __fma_rn(d[i], d[i + k], s0);
-                s1 = __fma_rn(d[i + 1], d[i + 1 + k], s1);
+        const int i0 = h * (kCorrTile / 2) + r;  // this thread's first i in the tile
+        double w[16];                            // ring: slot (j + s) & 15 holds d[i + g + 8 j] at step s
+#pragma unroll
+        for (int j = 0; j < 16; ++j) w[j] = d[i0 + g + 8 * j];
+        for (int m = 0; m < kCorrTile / 2 / 8; m += 16) {
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int i = i0 + 8 * (m + s);
+                const double di = d[i];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] = __fma_rn(di, w[(j + s) & 15], acc[j]);
+                w[s & 15] = d[i + g + 128];
             }
-            if (i < T) s0 = __fma_rn(d[i], d[i + k], s0);
         }
     }
-    if (k <= K) partial[(uint64_t)blockIdx.x * (K + 1) + k] = s0 + s1;
+    __syncthreads();
+    double (*red)[129] = reinterpret_cast<double (*)[129]>(d);  // [j][thread], padded
+#pragma unroll
+    for (int j = 0; j < 16; ++j) red[j][t] = acc[j];
+    __syncthreads();
+    // lag k = g + 8 j collects the 16 threads (h, r) with that (g, j), in a fixed order
+    const int k = t, kg = k & 7, kj = k >> 3;
+    double sum = 0.0;
+    for (int hh = 0; hh < 2; ++hh)
+        for (int rr = 0; rr < 8; ++rr) sum += red[kj][hh * 64 + kg * 8 + rr];
+    if (k <= K) partial[(uint64_t)blockIdx.x * (K + 1) + k] = sum;
 }
 
 }  // namespace nrng

@@ -52,6 +52,21 @@ def time_calls(g, method, n, mu, sigma, out, calls, warm=3, graph=False):
             "hbm_floor_frac": (8 * n / HBM) / (ms / 1e3)}
 
 
+def time_seq(g, method, n, out, calls):
+    stream = torch.cuda.current_stream()
+    g.normal_seq(method, out=out[:n])
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(calls):
+        g.normal_seq(method, out=out[:n])
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / calls
+    return {"n": n, "us_per_call": ms * 1e3, "normals_per_s": n / (ms / 1e3),
+            "hbm_floor_frac": (8 * n / HBM) / (ms / 1e3)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--calls", type=int, default=20)
@@ -79,6 +94,31 @@ def main():
     g = P.Generator(c.seed, c.streams)
     for m in c.methods + ("P2", "R", "R1"):
         res["C5shard_%s" % m] = time_calls(g, m, c.n, c.mu, c.sigma, big, 5)
+    # the sequential (RANN3-style, partition-invariant) mode at the shard
+    # shape: one whole-epoch call of 2^31 deviates, and 10^3 short calls of 10^4 deviates
+    for m in ("B1", "P"):
+        P.nrng_seq_reset(g.h)
+        res["seq_%s_bulk" % m] = time_seq(g, m, c.n, big, 3)
+        res["seq_%s_n10000" % m] = dict(time_seq(g, m, 10000, big, args.sweep_calls), calls=args.sweep_calls)
+    g.close()
+    # the validation reductions on 2^31 deviates (untimed in bench.py; HBM
+    # read-bound in principle: 16 GiB at the copy bandwidth is the floor)
+    import statistics
+    edges = [statistics.NormalDist().inv_cdf(i / 256) for i in range(1, 256)]
+    for name, fn in (("stats_256bins", lambda: P.stats(big, 0.0, edges)),
+                     ("gof_hist_2^20bins", lambda: P.gof_hist(big, 0.0, 1.0, 20)),
+                     ("serial_corr_lags100", lambda: P.serial_corr(big, 0.0, 100))):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        res["validate_%s" % name] = {"n": big.numel(), "ms_per_call": ms,
+                                      "read_gbs": 8 * big.numel() / (ms / 1e3) / 1e9,
+                                      "hbm_floor_frac": (8 * big.numel() / HBM) / (ms / 1e3)}
     print(json.dumps(res, indent=1))
 
 
