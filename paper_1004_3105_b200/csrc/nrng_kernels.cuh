@@ -1308,6 +1308,7 @@ __global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs,
 // (shared-memory int counters -> global u64 atomics).  A second kernel reduces the
 // block partials in a fixed order (deterministic sums).
 constexpr int kStatsThreads = 256;
+constexpr int kStatsCells = 2048;  // uniform cells over [edges[0], edges[K-2]] for the bin lookup
 __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(const double* __restrict__ x, uint64_t n,
                                                                       double center, const double* __restrict__ edges,
                                                                       int K, double* __restrict__ partial,
@@ -1315,8 +1316,25 @@ __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(const doub
     __shared__ double red[6][kStatsThreads / 32];
     __shared__ unsigned int sh[1024];
     __shared__ double se[1023];
+    __shared__ unsigned short cell[kStatsCells];  // edges <= the cell's left end (a lower bound)
     for (int b = threadIdx.x; b < K; b += blockDim.x) sh[b] = 0;
     for (int b = threadIdx.x; b < K - 1; b += blockDim.x) se[b] = edges[b];
+    __syncthreads();
+    // bin(v) = #edges <= v (K-1 edges, bins 0..K-1).  The cell of v gives a starting count that
+    // is corrected by short walks in both directions, so the result is exact whatever the
+    // rounding of the cell index (a binary search over 1023 edges per element cost 10 dependent
+    // shared loads; this costs one table load and one or two edge comparisons).
+    const double lo = se[0], hi = se[K - 2];
+    const double inv_w = hi > lo ? kStatsCells / (hi - lo) : 0.0;
+    for (int c = threadIdx.x; c < kStatsCells; c += blockDim.x) {
+        const double v = lo + (hi - lo) * c / kStatsCells;
+        int a = 0, b = K - 1;  // count of edges <= v by binary search (once per block)
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (v < se[mid]) b = mid; else a = mid + 1;
+        }
+        cell[c] = (unsigned short)a;
+    }
     __syncthreads();
     double s1 = 0, s2 = 0, s3 = 0, s4 = 0, mn = __longlong_as_double(0x7ff0000000000000ULL), mx = -mn;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -1329,12 +1347,19 @@ __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(const doub
         s4 += d2 * d2;
         mn = fmin(mn, v);
         mx = fmax(mx, v);
-        int lo = 0, hi = K - 1;  // first edge index with v < edge, in [0, K-1]
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (v < se[mid]) hi = mid; else lo = mid + 1;
+        int b;
+        if (v < lo) {
+            b = 0;
+        } else if (!(v < hi)) {  // v >= hi (and NaN, as the binary search placed it)
+            b = K - 1;
+        } else {
+            int c = (int)((v - lo) * inv_w);
+            c = c < 0 ? 0 : (c >= kStatsCells ? kStatsCells - 1 : c);
+            b = cell[c];
+            while (b > 0 && v < se[b - 1]) --b;
+            while (b < K - 1 && v >= se[b]) ++b;
         }
-        atomicAdd(&sh[lo], 1u);
+        atomicAdd(&sh[b], 1u);
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double vals[6] = {s1, s2, s3, s4, mn, mx};

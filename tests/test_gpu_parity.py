@@ -534,6 +534,25 @@ def test_above_2_32_outputs():
 
 # ---------------------------------------------------------------- validation reduction
 
+@pytest.mark.parametrize("K", [2, 3, 64, 256, 1024])
+def test_stats_histogram_bins_exact(K):
+    # bin(v) = #edges <= v, exactly (numpy searchsorted side='right'), for uneven edges, values
+    # equal to edges and their neighbours, and values outside the edge range
+    rng = np.random.default_rng(K)
+    edges = np.sort(np.concatenate([rng.standard_normal(K - 1 - (K - 1) // 3) * 2.0,
+                                    np.linspace(-0.5, 0.5, (K - 1) // 3)]))
+    x = np.concatenate([rng.standard_normal(300001) * 3.0, edges, np.nextafter(edges, -np.inf),
+                        np.nextafter(edges, np.inf), [-1e300, 1e300, edges[0] - 1e-3, edges[-1] + 1e-3]])
+    sums, hist = P.stats(torch.from_numpy(x).cuda(), 0.25, edges)
+    ref = np.bincount(np.searchsorted(edges, x, side="right"), minlength=K)
+    assert np.array_equal(host(hist), ref)
+    assert host(sums)[4] == x.min() and host(sums)[5] == x.max()
+    xm = x[:300001]  # moments without the +-1e300 extremes
+    sums, _ = P.stats(torch.from_numpy(xm).cuda(), 0.25, edges)
+    d, s = xm - 0.25, host(sums)
+    assert np.allclose(s[:4], [d.sum(), (d ** 2).sum(), (d ** 3).sum(), (d ** 4).sum()], rtol=1e-9, atol=1e-6)
+
+
 def test_stats_kernel_matches_oracle_stats():
     c = W.C1
     from scipy import stats as sps
