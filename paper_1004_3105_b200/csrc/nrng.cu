@@ -103,9 +103,22 @@ unsigned grid_for(uint32_t nstreams, int nw, int per_sm, int num_sms) {
 // blocks spread over all SMs.
 enum class Kind { BM1, BM2, BM3, POLAR, POLAR2, RATIO, RATIO1, UNIFORM };
 
+// The sequential mode's whole-epoch launches (equal quotas of whole 128-pair blocks, every
+// slot in range) run the same one-block-per-SM kernels with the epoch-layout store (EP).
+bool epoch_fast(const BulkParams& p) {
+    return p.aligned && p.log2E >= 7 && p.rem == 0 && p.q % 128 == 0 && p.n == 2 * p.units && p.shift == 0;
+}
+
 template <int V>
 void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
     const bool plain = p.aligned && p.log2E == 0;
+    if (epoch_fast(p) && ns >= (uint32_t)((V == 3 ? kTriWarps : kPwWarps) * h->num_sms)) {
+        if constexpr (V == 3)
+            b3_kernel<kTriWarps, true><<<h->num_sms, kTriWarps * 32, tri_smem(kTriWarps), st>>>(p);
+        else
+            pw_kernel<V, kPwWarps, true><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
+        return;
+    }
     if constexpr (V == 3) {
         if (plain && ns >= (uint32_t)(kTriWarps * h->num_sms)) {
             b3_kernel<kTriWarps><<<h->num_sms, kTriWarps * 32, tri_smem(kTriWarps), st>>>(p);
@@ -130,6 +143,10 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
 template <int M>
 void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
     constexpr int kPw = M == 1 ? 4 : 5;  // pw_kernel's P and P2 transforms
+    if (M == 1 && epoch_fast(p) && p.q + 1 < (1ull << 31) && ns >= (uint32_t)(kPwWarps * h->num_sms)) {
+        pw_kernel<4, kPwWarps, true><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
+        return;
+    }
     if ((M == 1 || NRNG_P2_PW) && p.aligned && p.log2E == 0 && p.q + 1 < (1ull << 31) &&
         ns >= (uint32_t)(kPwWarps * h->num_sms))
         pw_kernel<kPw, kPwWarps><<<h->num_sms, kPwWarps * 32, kPw == 5 ? r1_smem(kPwWarps) : bm_smem(kPwWarps), st>>>(p);
@@ -301,6 +318,10 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(pw_kernel<4, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
     occupancy(pw_kernel<5, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
     occupancy(pw_kernel<6, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(pw_kernel<1, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(pw_kernel<2, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(pw_kernel<4, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(b3_kernel<kTriWarps, true>, kTriWarps, tri_smem(kTriWarps));
     h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     occupancy(pw_kernel<7, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
     h->occ.ratio1 = occupancy(pw_kernel<7, kWarpsPerBlock>, kWarpsPerBlock, r1_smem(kWarpsPerBlock));

@@ -392,7 +392,7 @@ __device__ __forceinline__ void b3_iter(uint64_t* lb, const TParams& tp, const T
 }
 
 // Aligned, plain-layout B3 calls (the dispatcher sends the rest to bm_kernel<3>).
-template <int NW>
+template <int NW, bool EP = false>  // EP: the sequential mode's epoch layout (see pw_kernel)
 __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -420,18 +420,25 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
         const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
         const uint32_t nit = (uint32_t)(safe_cnt / 128);  // full 4-row iterations (a 32-bit count: no
-        double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;  // per-iteration
+        double2* o = EP ? reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, 0) + lane
+                        : reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;  // per-iteration
+        auto adv = [&](uint32_t itn) {  // o -> the first pair of iteration itn (+ lane)
+            if constexpr (EP)
+                o = reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, 128ull * itn) + lane;
+            else
+                o += 128;
+        };
         uint64_t* const lb = buf + 3 * lane;
         for (uint32_t it = 0;;) {  // unrolled over the 3 phases of the 12-row window
             if (it == nit) break;
             b3_iter<0>(lb, p.tp, tab, scr, lane, lt, o);
-            o += 128;
+            adv(it + 1);
             if (++it == nit) break;
             b3_iter<1>(lb, p.tp, tab, scr, lane, lt, o);
-            o += 128;
+            adv(it + 1);
             if (++it == nit) break;
             b3_iter<2>(lb, p.tp, tab, scr, lane, lt, o);
-            o += 128;
+            adv(it + 1);
             ++it;
         }
         const uint32_t d0 = 4 * kTriRow * (nit % 3);
@@ -446,7 +453,8 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
             double x[1], y[1];
             b3_pairs<1>(w1, w2, w3, p.tp, tab, x, y);
             if ((uint64_t)lane < qk2.cnt - j0)
-                store_pair(p.out, 2 * (qk2.off + j0 + lane), p.shift, p.n, x[0], y[0], true);
+                store_pair(p.out, 2 * (EP ? pair_slot(p, qk2.off, k, j0 + lane) : qk2.off + j0 + lane), p.shift, p.n,
+                           x[0], y[0], true);
             __syncwarp();
             ps.advance(1);
         }
@@ -815,11 +823,11 @@ __device__ __forceinline__ void pw_bm_block(const PwPtrs& pp, const TParams& tp,
 
 // One Polar step (128 candidates, one block) at compile-time base K; returns whether the
 // quota was reached (exact stop: `used` = candidates consumed of this block).
-template <int M, int K>
+template <int M, int K, bool EP = false>
 __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& tp, const Tables& tab,
                                                const BulkParams& p, const Quota& qk, double2* o, bool direct,
                                                uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt,
-                                               double* scr) {
+                                               double* scr, uint32_t k = 0) {
     uint64_t wa[kPU], wb[kPU];
     pw_gen_c<kPU, K>(pp, wa, wb);
     PolarCand c[kPU];
@@ -834,7 +842,19 @@ __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& 
         p2_transform_compact<kPU>(c, ok, tp, tab, scr, lane, lt, ox, oy);
     else
         polar_transform<kPU>(c, tp, tab, ox, oy);
-    if (direct) {
+    if (EP) {  // the sequential mode's epoch layout (whole epochs: every pair is in range)
+        // a step's <= 128 pairs span at most two epoch chunks of E >= 128 pairs: pair j goes to
+        // chunk e0's start + (j - e0 E), plus the jump to the next chunk once j - e0 E >= E
+        const uint32_t e0 = acc >> p.log2E, jb = e0 << p.log2E, E = 1u << p.log2E;
+        double2* const ob = reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, jb);
+        const uint64_t jump = ((uint64_t)p.S << p.log2E) - E;
+#pragma unroll
+        for (int u = 0; u < kPU; ++u) {
+            const uint32_t jj = acc + __popc(m[u] & lt) - jb;
+            if ((m[u] >> lane) & 1u) __stcs(ob + jj + (jj >= E ? jump : 0), make_double2(ox[u], oy[u]));
+            acc += __popc(m[u]);
+        }
+    } else if (direct) {
 #pragma unroll
         for (int u = 0; u < kPU; ++u) {
             if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), make_double2(ox[u], oy[u]));
@@ -900,7 +920,10 @@ __device__ __forceinline__ bool pw_ratio1_block(const PwPtrs& pp, const TParams&
     return stop;
 }
 
-template <int M, int NW>
+// EP: the sequential mode's epoch layout (pair j of stream k at slot (j >> log2E) S E + k E +
+// (j & (E-1)), E >= 128 a power of two, equal quotas, whole 128-pair blocks): each block's 128
+// pairs are still contiguous, only the block pointer (and Polar's per-pair slot) changes.
+template <int M, int NW, bool EP = false>
 __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -932,27 +955,34 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
             // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
             const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
             const uint32_t nblk = (uint32_t)(safe_cnt / 128);
-            double2* o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
+            double2* o = EP ? reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, 0) + lane
+                            : reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
             uint32_t b = 0;
+            auto adv = [&](uint32_t bn) {  // o -> the first pair of block bn (+ lane)
+                if constexpr (EP)
+                    o = reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, 128ull * bn) + lane;
+                else
+                    o += 128;
+            };
             // B2: unrolled over the 4 block positions (compile-time window offsets); B1: one
             // block body with the offsets from the constant bank (measured faster for B1: the
             // unrolled body issued 16% fewer instructions but scheduled worse, 79% vs 92% of
             // the issue bound)
             if constexpr (M == 2 || (M == 1 && NRNG_B1_UNROLL)) while (b < nblk) {  // 4 block positions per pass, compile-time window offsets
                 pw_bm_block<M, 0>(pp, p.tp, tab, o);
-                o += 128;
+                adv(b + 1);
                 if (++b == nblk) break;
                 pw_bm_block<M, 256>(pp, p.tp, tab, o);
-                o += 128;
+                adv(b + 1);
                 if (++b == nblk) break;
                 pw_bm_block<M, 512>(pp, p.tp, tab, o);
-                o += 128;
+                adv(b + 1);
                 if (++b == nblk) break;
                 pw_bm_block<M, 768>(pp, p.tp, tab, o);
-                o += 128;
+                adv(b + 1);
                 ++b;
             }
-            else for (; b < nblk; ++b, o += 128) {
+            else for (; b < nblk; ++b, adv(b)) {
                 uint64_t wu[4], wv[4];
                 pw_gen_r<4>(pp, b & 3, wu, wv);
                 double x[4], y[4];
@@ -974,7 +1004,8 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
                 else
                     b2_pairs<1>(wu, wv, p.tp, tab, x, y);
                 if ((uint64_t)lane < qk.cnt - j0)
-                    store_pair(p.out, 2 * (qk.off + j0 + lane), p.shift, p.n, x[0], y[0], true);
+                    store_pair(p.out, 2 * (EP ? pair_slot(p, qk.off, k, j0 + lane) : qk.off + j0 + lane), p.shift, p.n,
+                               x[0], y[0], true);
                 __syncwarp();
                 K = (K + 64) & kWinMask;
             }
@@ -1018,13 +1049,13 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
             const uint32_t cnt = (uint32_t)qk.cnt;
             uint32_t acc = 0, blocks = 0, usedc = 0;
             for (;;) {
-                if (pw_polar_block<M, 0>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr)) break;
+                if (pw_polar_block<M, 0, EP>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
                 ++blocks;
-                if (pw_polar_block<M, 256>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr)) break;
+                if (pw_polar_block<M, 256, EP>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
                 ++blocks;
-                if (pw_polar_block<M, 512>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr)) break;
+                if (pw_polar_block<M, 512, EP>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
                 ++blocks;
-                if (pw_polar_block<M, 768>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr)) break;
+                if (pw_polar_block<M, 768, EP>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
                 ++blocks;
             }
             used = (uint64_t)kBlk * blocks + 2 * usedc;

@@ -617,6 +617,23 @@ def test_sequential_mode_partition_invariant(method):
     assert P.nrng_seq_buffered(a.h) == 3 * ep - total
 
 
+@pytest.mark.parametrize("method,E", [("B1", 128), ("B2", 256), ("B3", 128), ("P", 128), ("P", 512)])
+def test_sequential_mode_wide_epoch_kernels(method, E):
+    # >= 16 x 148 streams: whole epochs go through the one-block-per-SM kernels with the
+    # epoch-layout store (EP); against the oracle's epoch sequence, and partition-invariant
+    S = 2400
+    ep = 2 * S * E
+    total = 3 * ep + 4321
+    a, b = P.Generator(31, S), P.Generator(31, S)
+    P.nrng_seq_configure(a.h, E)
+    P.nrng_seq_configure(b.h, E)
+    one = host(a.normal_seq(method, total, -0.5, 1.5))
+    parts = [host(b.normal_seq(method, m, -0.5, 1.5)) for m in (ep + 7, 2 * ep - 7, total - 3 * ep)]
+    assert np.array_equal(one, np.concatenate(parts))
+    o = _oracle_seq(31, S, E, method, total, -0.5, 1.5)
+    assert np.max(np.abs(one - o)) <= tol_for(method)
+
+
 def test_sequential_mode_params_and_host_output():
     S = 128
     g = P.Generator(3, S)
