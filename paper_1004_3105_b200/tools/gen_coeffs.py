@@ -206,6 +206,9 @@ def main():
     body.append("__constant__ double kB2Sin[4] = {%s};  // S1, S3, S5, S7" % ", ".join(v.hex() for v in sin_c))
     body.append("// cos y ~ C0 + C2 y^2 + C4 y^4 + C6 y^6")
     body.append("__constant__ double kB2Cos[4] = {%s};  // C0, C2, C4, C6" % ", ".join(v.hex() for v in cos_c))
+    body.append("// the same polynomials times 2 (exact): sincos16 carries (2s, 2c), see sincos16_x2")
+    body.append("__constant__ double kB2Sin2[4] = {%s};" % ", ".join(math.ldexp(v, 1).hex() for v in sin_c))
+    body.append("__constant__ double kB2Cos2[4] = {%s};" % ", ".join(math.ldexp(v, 1).hex() for v in cos_c))
     body.append("// h(v) ~ sum_j kH[j] v^j")
     body.append("__constant__ double kH[16] = {")
     body += ["    %s," % v.hex() for v in h_c]
