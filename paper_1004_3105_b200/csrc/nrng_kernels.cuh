@@ -4,6 +4,8 @@
 // thread; the lag structure gives 256 independent words per refill).  Warps stride
 // over streams, persistent grid sized to the SM count x resident blocks.
 #pragma once
+#include <utility>
+
 #include "nrng_device.cuh"
 
 namespace nrng {
@@ -685,6 +687,9 @@ constexpr int kPwWarps = NRNG_PW_WARPS;
 #endif
 __device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
 
+#ifndef NRNG_PW_NOMIRROR
+#define NRNG_PW_NOMIRROR 1  // compile-time generator: no mirror; straddling runs read through lane-wrapped pointers
+#endif
 struct PwLane {  // physical offsets of this lane's words in a row whose base is 0
     uint32_t a0, a1, b0, b1, d0, d1;
 };
@@ -699,23 +704,36 @@ __device__ __forceinline__ PwLane pw_lane(int lane) {
 // The source runs are masked once per call (a run of R rows may extend up to 255 words past
 // 1023, into the mirror), so every row is the same four per-lane pointers plus an immediate.
 // All loads are issued before any store (all sources are older than the rows: 64 R <= 273).
-template <int R>
+template <int R, bool kNoMirror = NRNG_PW_NOMIRROR>
 __device__ __forceinline__ void pw_gen(uint64_t* buf, uint32_t K, const PwLane& o, uint64_t (&w0)[R],
-                                       uint64_t (&w1)[R]) {
+                                       uint64_t (&w1)[R], int lane) {
     static_assert(64 * R <= kLagS && 64 * R <= kMirror, "rows of one call must be independent");
-    const int ka = (int)((K + (kWin - kLagR)) & kWinMask) - (kWin - kLagR);  // multiple of 64
-    const int kb = (int)((K + (kWin - kLagS)) & kWinMask) - (kWin - kLagS);
-    const uint64_t* pa0 = buf + (ka + (int)o.a0);
-    const uint64_t* pa1 = buf + (ka + (int)o.a1);
-    const uint64_t* pb0 = buf + (kb + (int)o.b0);
-    const uint64_t* pb1 = buf + (kb + (int)o.b1);
     uint64_t a0[R], a1[R], b0[R], b1[R];
+    if constexpr (kNoMirror) {
+        // every source position wrapped per lane (the short-call tail path: no mirror reads)
+        const uint32_t l2 = 2 * lane;
 #pragma unroll
-    for (int t = 0; t < R; ++t) {
-        a0[t] = pa0[64 * t];
-        a1[t] = pa1[64 * t];
-        b0[t] = pb0[64 * t];
-        b1[t] = pb1[64 * t];
+        for (int t = 0; t < R; ++t) {
+            const uint32_t pa = K + 64 * t + (kWin - kLagR) + l2, pb = K + 64 * t + (kWin - kLagS) + l2;
+            a0[t] = buf[swz(pa & kWinMask)];
+            a1[t] = buf[swz((pa + 1) & kWinMask)];
+            b0[t] = buf[swz(pb & kWinMask)];
+            b1[t] = buf[swz((pb + 1) & kWinMask)];
+        }
+    } else {
+        const int ka = (int)((K + (kWin - kLagR)) & kWinMask) - (kWin - kLagR);  // multiple of 64
+        const int kb = (int)((K + (kWin - kLagS)) & kWinMask) - (kWin - kLagS);
+        const uint64_t* pa0 = buf + (ka + (int)o.a0);
+        const uint64_t* pa1 = buf + (ka + (int)o.a1);
+        const uint64_t* pb0 = buf + (kb + (int)o.b0);
+        const uint64_t* pb1 = buf + (kb + (int)o.b1);
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            a0[t] = pa0[64 * t];
+            a1[t] = pa1[64 * t];
+            b0[t] = pb0[64 * t];
+            b1[t] = pb1[64 * t];
+        }
     }
     uint64_t* pd0 = buf + (K + o.d0);
     uint64_t* pd1 = buf + (K + o.d1);
@@ -726,7 +744,7 @@ __device__ __forceinline__ void pw_gen(uint64_t* buf, uint32_t K, const PwLane& 
         pd0[64 * t] = w0[t];
         pd1[64 * t] = w1[t];
     }
-    if (K < (uint32_t)kMirror) {  // rows in [0, 256): mirrored at +1024
+    if (!kNoMirror && K < (uint32_t)kMirror) {  // rows in [0, 256): mirrored at +1024
 #pragma unroll
         for (int t = 0; t < R; ++t) {
             pd0[kWin + 64 * t] = w0[t];
@@ -740,22 +758,58 @@ __device__ __forceinline__ void pw_gen(uint64_t* buf, uint32_t K, const PwLane& 
 struct PwPtrs {
     const uint64_t *a0, *a1, *b0, *b1;
     uint64_t *d0, *d1;
+    // the same source pointers minus one window (1024 words) on the lanes whose word of the one
+    // row per lag that straddles the window's end lies past it (NRNG_PW_NOMIRROR): lag-607 run
+    // at position 993 (+2l, +1: lanes >= 16 / >= 15), lag-273 run at 1007 (lanes >= 9 / >= 8)
+    const uint64_t *a0x, *a1x, *b0x, *b1x;
 };
-__device__ __forceinline__ PwPtrs pw_ptrs(uint64_t* buf, const PwLane& o) {
-    return PwPtrs{buf + o.a0, buf + o.a1, buf + o.b0, buf + o.b1, buf + o.d0, buf + o.d1};
+__device__ __forceinline__ PwPtrs pw_ptrs(uint64_t* buf, const PwLane& o, int lane = 0) {
+    return PwPtrs{buf + o.a0, buf + o.a1, buf + o.b0, buf + o.b1, buf + o.d0, buf + o.d1,
+                  buf + o.a0 - (lane >= 16 ? kWin : 0), buf + o.a1 - (lane >= 15 ? kWin : 0),
+                  buf + o.b0 - (lane >= 9 ? kWin : 0), buf + o.b1 - (lane >= 8 ? kWin : 0)};
 }
+// Row T of a compile-time block at K without the mirror: run starts (logical window positions of
+// lane 0's words) past the end are read one window lower; the one straddling run per lag goes
+// through the lane-wrapped pointers.
+template <int K, int T>
+__device__ __forceinline__ void pw_load_row(const PwPtrs& pp, uint64_t& a0, uint64_t& a1, uint64_t& b0, uint64_t& b1) {
+    constexpr int ka = ((K + (kWin - kLagR)) & kWinMask) - (kWin - kLagR);
+    constexpr int kb = ((K + (kWin - kLagS)) & kWinMask) - (kWin - kLagS);
+    constexpr int sa = ((K + (kWin - kLagR)) & kWinMask) + 64 * T;
+    constexpr int sb = ((K + (kWin - kLagS)) & kWinMask) + 64 * T;
+    static_assert((sa >= kWin || sa + 64 <= kWin || sa == kWin - 31) &&
+                      (sb >= kWin || sb + 64 <= kWin || sb == kWin - 17),
+                  "the lane-wrapped pointers cover exactly these straddling runs");
+    constexpr int oa = ka + 64 * T - (sa >= kWin ? kWin : 0);
+    constexpr int ob = kb + 64 * T - (sb >= kWin ? kWin : 0);
+    constexpr bool xa = sa < kWin && sa + 64 > kWin, xb = sb < kWin && sb + 64 > kWin;
+    a0 = (xa ? pp.a0x : pp.a0)[oa];
+    a1 = (xa ? pp.a1x : pp.a1)[oa];
+    b0 = (xb ? pp.b0x : pp.b0)[ob];
+    b1 = (xb ? pp.b1x : pp.b1)[ob];
+}
+template <int K, int R, int... T>
+__device__ __forceinline__ void pw_load_rows(const PwPtrs& pp, uint64_t (&a0)[R], uint64_t (&a1)[R], uint64_t (&b0)[R],
+                                             uint64_t (&b1)[R], std::integer_sequence<int, T...>) {
+    (pw_load_row<K, T>(pp, a0[T], a1[T], b0[T], b1[T]), ...);
+}
+
 template <int R, int K>
 __device__ __forceinline__ void pw_gen_c(const PwPtrs& pp, uint64_t (&w0)[R], uint64_t (&w1)[R]) {
     static_assert(64 * R <= kLagS && 64 * R <= kMirror && K % 64 == 0 && K + 64 * R <= kWin, "row geometry");
     constexpr int ka = ((K + (kWin - kLagR)) & kWinMask) - (kWin - kLagR);
     constexpr int kb = ((K + (kWin - kLagS)) & kWinMask) - (kWin - kLagS);
     uint64_t a0[R], a1[R], b0[R], b1[R];
+    if constexpr (NRNG_PW_NOMIRROR) {
+        pw_load_rows<K>(pp, a0, a1, b0, b1, std::make_integer_sequence<int, R>{});
+    } else {
 #pragma unroll
-    for (int t = 0; t < R; ++t) {
-        a0[t] = pp.a0[ka + 64 * t];
-        a1[t] = pp.a1[ka + 64 * t];
-        b0[t] = pp.b0[kb + 64 * t];
-        b1[t] = pp.b1[kb + 64 * t];
+        for (int t = 0; t < R; ++t) {
+            a0[t] = pp.a0[ka + 64 * t];
+            a1[t] = pp.a1[ka + 64 * t];
+            b0[t] = pp.b0[kb + 64 * t];
+            b1[t] = pp.b1[kb + 64 * t];
+        }
     }
 #pragma unroll
     for (int t = 0; t < R; ++t) {
@@ -763,7 +817,7 @@ __device__ __forceinline__ void pw_gen_c(const PwPtrs& pp, uint64_t (&w0)[R], ui
         w1[t] = a1[t] + b1[t];
         pp.d0[K + 64 * t] = w0[t];
         pp.d1[K + 64 * t] = w1[t];
-        if (K < kMirror) {
+        if (!NRNG_PW_NOMIRROR && K < kMirror) {
             pp.d0[K + kWin + 64 * t] = w0[t];
             pp.d1[K + kWin + 64 * t] = w1[t];
         }
@@ -931,7 +985,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     __syncthreads();
     uint64_t* const buf = smem + warp * kWinAlloc;
     const PwLane ol = pw_lane(lane);
-    const PwPtrs pp = pw_ptrs(buf, ol);
+    const PwPtrs pp = pw_ptrs(buf, ol, lane);
     const unsigned lt = lanemask_lt(lane);
     double* const scr = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + 32 * warp;  // M = 5, 7
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
@@ -997,7 +1051,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
             uint32_t K = (256 * b) & kWinMask;
             for (uint64_t j0 = 128ull * b; j0 < qk.cnt; j0 += 32) {  // last rows, partial, unsafe pair
                 uint64_t wu[1], wv[1];
-                pw_gen<1>(buf, K, ol, wu, wv);
+                pw_gen<1, M != 1 && NRNG_PW_NOMIRROR>(buf, K, ol, wu, wv, lane);  // B1 keeps its mirror
                 double x[1], y[1];
                 if (M == 1)
                     b1_pairs<1>(wu, wv, p.tp, tab, x, y);
