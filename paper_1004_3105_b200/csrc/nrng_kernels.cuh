@@ -1051,7 +1051,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
             uint32_t K = (256 * b) & kWinMask;
             for (uint64_t j0 = 128ull * b; j0 < qk.cnt; j0 += 32) {  // last rows, partial, unsafe pair
                 uint64_t wu[1], wv[1];
-                pw_gen<1, M != 1 && NRNG_PW_NOMIRROR>(buf, K, ol, wu, wv, lane);  // B1 keeps its mirror
+                pw_gen<1, (M != 1 || NRNG_B1_UNROLL) && NRNG_PW_NOMIRROR>(buf, K, ol, wu, wv, lane);  // B1's runtime body keeps its mirror
                 double x[1], y[1];
                 if (M == 1)
                     b1_pairs<1>(wu, wv, p.tp, tab, x, y);
