@@ -147,6 +147,10 @@ void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t 
         pw_kernel<4, kPwWarps, true><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
         return;
     }
+    if (M == 2 && epoch_fast(p) && p.q + 1 < (1ull << 31) && ns >= (uint32_t)(kBigBlockPolar * h->num_sms)) {
+        polar_kernel<kBigBlockPolar, 2, true><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
+        return;
+    }
     if ((M == 1 || NRNG_P2_PW) && p.aligned && p.log2E == 0 && p.q + 1 < (1ull << 31) &&
         ns >= (uint32_t)(kPwWarps * h->num_sms))
         pw_kernel<kPw, kPwWarps><<<h->num_sms, kPwWarps * 32, kPw == 5 ? r1_smem(kPwWarps) : bm_smem(kPwWarps), st>>>(p);
@@ -327,6 +331,7 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     h->occ.ratio1 = occupancy(pw_kernel<7, kWarpsPerBlock>, kWarpsPerBlock, r1_smem(kWarpsPerBlock));
     occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     occupancy(polar_kernel<kBigBlockPolar, 2>, kBigBlockPolar, polar_smem(kBigBlockPolar));
+    occupancy(polar_kernel<kBigBlockPolar, 2, true>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     h->occ.uni = occupancy(uniform_kernel, kWarpsPerBlock, kUniSmem);
     h->occ.mask = occupancy(polar_mask_kernel, kWarpsPerBlock, kUniSmem);
     h->occ.init = occupancy(init_kernel, kWarpsPerBlock, kInitSmem);

@@ -533,7 +533,7 @@ __device__ __forceinline__ uint32_t polar_rank(const bool (&ok)[kPU], unsigned (
     return used;
 }
 
-template <int NW, int M>
+template <int NW, int M, bool EP = false>  // EP: the sequential mode's whole-epoch layout (see pw_kernel)
 __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
         lfg_load(L, rk, C, lane);
         prefetch_state<2>(p, k + gridDim.x * NW, lane);
         const bool fast = p.aligned && 2 * (qk.off + qk.cnt) <= p.n;
-        const bool direct = fast && p.log2E == 0;
+        const bool direct = fast && (EP || p.log2E == 0);
         const bool phased = direct && qk.cnt < (1ull << 31);
         if (phased) {
             // Phased steady state: every step but the stream's last consumes exactly one
@@ -589,10 +589,22 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                     p2_transform_compact<kPU>(c, ok, p.tp, tab, scr, lane, lt, ox, oy);
                 else
                     polar_transform<kPU>(c, p.tp, tab, ox, oy);
+                if constexpr (EP) {  // at most two epoch chunks per step (as pw_polar_block)
+                    const uint32_t e0 = acc >> p.log2E, jb = e0 << p.log2E, E = 1u << p.log2E;
+                    double2* const ob = reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, jb);
+                    const uint64_t jump = ((uint64_t)p.S << p.log2E) - E;
 #pragma unroll
-                for (int u = 0; u < kPU; ++u) {
-                    if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), make_double2(ox[u], oy[u]));
-                    acc += __popc(m[u]);
+                    for (int u = 0; u < kPU; ++u) {
+                        const uint32_t jj = acc + __popc(m[u] & lt) - jb;
+                        if ((m[u] >> lane) & 1u) __stcs(ob + jj + (jj >= E ? jump : 0), make_double2(ox[u], oy[u]));
+                        acc += __popc(m[u]);
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < kPU; ++u) {
+                        if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), make_double2(ox[u], oy[u]));
+                        acc += __popc(m[u]);
+                    }
                 }
                 __syncwarp();
                 if (stop) {

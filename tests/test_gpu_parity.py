@@ -617,7 +617,7 @@ def test_sequential_mode_partition_invariant(method):
     assert P.nrng_seq_buffered(a.h) == 3 * ep - total
 
 
-@pytest.mark.parametrize("method,E", [("B1", 128), ("B2", 256), ("B3", 128), ("P", 128), ("P", 512)])
+@pytest.mark.parametrize("method,E", [("B1", 128), ("B2", 256), ("B3", 128), ("P", 128), ("P", 512), ("P2", 128)])
 def test_sequential_mode_wide_epoch_kernels(method, E):
     # >= 16 x 148 streams: whole epochs go through the one-block-per-SM kernels with the
     # epoch-layout store (EP); against the oracle's epoch sequence, and partition-invariant
