@@ -697,6 +697,9 @@ constexpr int kPwWarps = NRNG_PW_WARPS;
 #ifndef NRNG_B1_UNROLL
 #define NRNG_B1_UNROLL 0
 #endif
+#ifndef NRNG_B1_MIRROR_BRANCH
+#define NRNG_B1_MIRROR_BRANCH 1
+#endif
 __device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
 
 #ifndef NRNG_PW_NOMIRROR
@@ -863,6 +866,17 @@ __device__ __forceinline__ void pw_gen_r(const PwPtrs& pp, uint32_t ph, uint64_t
         pp.d0[K + 64 * t] = w0[t];
         pp.d1[K + 64 * t] = w1[t];
     }
+#if NRNG_B1_MIRROR_BRANCH  // a real branch: the mirror stores are skipped in 3 blocks of 4
+    if (__builtin_expect(ph == 0, 0)) {
+        asm volatile("" ::: "memory");
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            pp.d0[kWin + 64 * t] = w0[t];
+            pp.d1[kWin + 64 * t] = w1[t];
+        }
+        __syncwarp();
+    }
+#else
     if (ph == 0) {
 #pragma unroll
         for (int t = 0; t < R; ++t) {
@@ -870,6 +884,7 @@ __device__ __forceinline__ void pw_gen_r(const PwPtrs& pp, uint32_t ph, uint64_t
             pp.d1[kWin + 64 * t] = w1[t];
         }
     }
+#endif
 }
 
 // One steady-state B1/B2 block (128 pairs) at compile-time window base K.
