@@ -1165,7 +1165,10 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
 // words are loaded together (ILP) and transformed as one 4-wide batch.  Only the words
 // actually used are touched; unconsumed words of a Polar chunk are not written back.
 constexpr int kTinyThreads = 128;
-constexpr uint64_t kTinyMaxPairs = 32;  // per-stream quota routed here
+#ifndef NRNG_TINY_MAX
+#define NRNG_TINY_MAX 32
+#endif
+constexpr uint64_t kTinyMaxPairs = NRNG_TINY_MAX;  // per-stream quota routed here
 
 // x_{n+t}, t < CW, where ring position a holds x_{n-607} (valid for CW <= 273).
 template <int CW>
@@ -1293,6 +1296,91 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
         j += take;
     }
     p.count[k] = C + used;
+}
+
+// ------------------------------------------------------------------ mid-size quotas
+// Per-stream quotas of a few dozen pairs (the C4 sweep at n = 2^21..2^23 over 2^16 streams):
+// too short for the shared-memory window (the full 4.8 KB state load would dominate) and too
+// long for one thread per stream (whose 8-byte ring accesses are uncoalesced).  One WARP owns a
+// stream and steps through the HBM ring in the canonical layout, 32 units per step (a pair for
+// B1/B2, a candidate for Polar; lane l takes the step's words 2l, 2l+1): x_{C+i} =
+// ring[(C+i) mod 607] + ring[(C+i+334) mod 607], written back in place.  Within a step the
+// lanes' words are 64 apart at most (< 273), so every source is older than the step: loads
+// first, then the new words, then a __syncwarp before the next step reads them.  Only the words
+// a call consumes are read or written (Polar's exact stop leaves later candidates untouched).
+constexpr int kMidWarps = 4;
+#ifndef NRNG_MID_MIN
+#define NRNG_MID_MIN 12
+#endif
+#ifndef NRNG_MID_MAX
+#define NRNG_MID_MAX 128
+#endif
+constexpr uint64_t kMidMinPairs = NRNG_MID_MIN, kMidMaxPairs = NRNG_MID_MAX;  // per-stream quota routed here
+
+template <int V>  // 1, 2 = B1, B2; 4 = Polar
+__global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
+    __shared__ double2 tabs[kTabBytes / 16];
+    const Tables tab = load_tables(tabs);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt(lane);
+    for (uint32_t k = p.s_begin + blockIdx.x * kMidWarps + warp; k < p.s_end; k += gridDim.x * kMidWarps) {
+        const Quota qk = quota(p.q, p.rem, k);
+        if (qk.cnt == 0) continue;
+        const uint64_t C = p.count[k];
+        uint64_t* r = p.ring + (uint64_t)k * kPitch;
+        const uint32_t c0 = (uint32_t)(C % kLagR);
+        uint32_t i0 = 0;  // words of the call consumed before this step
+        uint32_t j = 0;   // pairs delivered
+        while (j < qk.cnt) {
+            // this lane's two words: call-relative i0 + 2l, +1
+            uint32_t pa = c0 + i0 + 2 * lane, pb = pa + (kLagR - kLagS);
+            pa %= kLagR;
+            pb %= kLagR;
+            const uint32_t pa1 = pa + 1 == (uint32_t)kLagR ? 0 : pa + 1, pb1 = pb + 1 == (uint32_t)kLagR ? 0 : pb + 1;
+            const uint64_t w0 = r[pa] + r[pb], w1 = r[pa1] + r[pb1];
+            uint32_t words;  // words this step consumes (stores only those)
+            if constexpr (V <= 2) {
+                const uint64_t wu[1] = {w0}, wv[1] = {w1};
+                double x[1], y[1];
+                if (V == 1)
+                    b1_pairs<1>(wu, wv, p.tp, tab, x, y);
+                else
+                    b2_pairs<1>(wu, wv, p.tp, tab, x, y);
+                const uint32_t take = qk.cnt - j < 32 ? (uint32_t)(qk.cnt - j) : 32u;
+                if ((uint32_t)lane < take)
+                    store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + lane), p.shift, p.n, x[0], y[0], p.aligned);
+                words = 2 * take;
+                j += take;
+            } else {
+                PolarCand c[1];
+                const bool ok = polar_candidate(w0, w1, c[0]);
+                double x[1], y[1];
+                polar_transform<1>(c, p.tp, tab, x, y);
+                const unsigned m = __ballot_sync(kFull, ok);
+                const uint32_t need = (uint32_t)(qk.cnt - j), rank = __popc(m & lt);
+                if (ok && rank < need)
+                    store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + rank), p.shift, p.n, x[0], y[0], p.aligned);
+                const uint32_t got = __popc(m);
+                if (got >= need) {  // exact stop: nothing after the need-th accept is consumed
+                    const unsigned last = __ballot_sync(kFull, ok && rank == need - 1);
+                    words = 2 * (uint32_t)__ffs(last);
+                    j += need;
+                } else {
+                    words = 64;
+                    j += got;
+                }
+            }
+            if ((uint32_t)(2 * lane) < words) {  // write back the consumed words in place
+                r[pa] = w0;
+                r[pa1] = w1;
+            }
+            i0 += words;
+            __syncwarp();
+        }
+        if (lane == 0) p.count[k] = C + i0;
+        __syncwarp();
+    }
 }
 
 // ------------------------------------------------------------------ test hooks
