@@ -164,12 +164,15 @@ void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t 
 cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st) {
     uint32_t ns = p.s_end - p.s_begin;
     const uint64_t qmax = p.q + (p.rem ? 1 : 0);
-    if ((kind == Kind::BM1 || kind == Kind::BM2 || kind == Kind::POLAR) && qmax >= kMidMinPairs &&
-        qmax <= kMidMaxPairs && NRNG_MID_MAX > 0) {
+    if (kind != Kind::UNIFORM && qmax >= kMidMinPairs && qmax <= kMidMaxPairs && NRNG_MID_MAX > 0) {
         const unsigned grid = (unsigned)std::min<uint64_t>((ns + kMidWarps - 1) / kMidWarps, (uint64_t)h->num_sms * 16);
         switch (kind) {
             case Kind::BM1: mid_kernel<1><<<grid, kMidWarps * 32, 0, st>>>(p); break;
             case Kind::BM2: mid_kernel<2><<<grid, kMidWarps * 32, 0, st>>>(p); break;
+            case Kind::BM3: mid_kernel<3><<<grid, kMidWarps * 32, 0, st>>>(p); break;
+            case Kind::POLAR2: mid_kernel<5><<<grid, kMidWarps * 32, 0, st>>>(p); break;
+            case Kind::RATIO:   // R1's pretests change no output: its mid-size calls are R's
+            case Kind::RATIO1: mid_kernel<6><<<grid, kMidWarps * 32, 0, st>>>(p); break;
             default: mid_kernel<4><<<grid, kMidWarps * 32, 0, st>>>(p); break;
         }
         h->launches += 1;

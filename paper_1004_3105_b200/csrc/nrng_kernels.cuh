@@ -1317,7 +1317,7 @@ constexpr int kMidWarps = 4;
 #endif
 constexpr uint64_t kMidMinPairs = NRNG_MID_MIN, kMidMaxPairs = NRNG_MID_MAX;  // per-stream quota routed here
 
-template <int V>  // 1, 2 = B1, B2; 4 = Polar
+template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2; 6 = R (units: normals, one per accept)
 __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
     __shared__ double2 tabs[kTabBytes / 16];
     const Tables tab = load_tables(tabs);
@@ -1333,34 +1333,71 @@ __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
         uint32_t i0 = 0;  // words of the call consumed before this step
         uint32_t j = 0;   // pairs delivered
         while (j < qk.cnt) {
-            // this lane's two words: call-relative i0 + 2l, +1
-            uint32_t pa = c0 + i0 + 2 * lane, pb = pa + (kLagR - kLagS);
-            pa %= kLagR;
-            pb %= kLagR;
-            const uint32_t pa1 = pa + 1 == (uint32_t)kLagR ? 0 : pa + 1, pb1 = pb + 1 == (uint32_t)kLagR ? 0 : pb + 1;
-            const uint64_t w0 = r[pa] + r[pb], w1 = r[pa1] + r[pb1];
+            // this lane's words: call-relative i0 + per l + t (per = 3 for B3, else 2)
+            constexpr int per = V == 3 ? 3 : 2;
+            uint32_t pa[per], pb[per];
+            uint64_t w[per];
+            {
+                uint32_t a = (c0 + i0 + per * lane) % kLagR;
+                uint32_t b = a + (kLagR - kLagS);
+                b = b >= (uint32_t)kLagR ? b - kLagR : b;
+#pragma unroll
+                for (int t = 0; t < per; ++t) {
+                    pa[t] = a;
+                    pb[t] = b;
+                    a = a + 1 == (uint32_t)kLagR ? 0 : a + 1;
+                    b = b + 1 == (uint32_t)kLagR ? 0 : b + 1;
+                }
+                uint64_t xa[per], xb[per];
+#pragma unroll
+                for (int t = 0; t < per; ++t) xa[t] = r[pa[t]], xb[t] = r[pb[t]];
+#pragma unroll
+                for (int t = 0; t < per; ++t) w[t] = xa[t] + xb[t];
+            }
             uint32_t words;  // words this step consumes (stores only those)
-            if constexpr (V <= 2) {
-                const uint64_t wu[1] = {w0}, wv[1] = {w1};
+            if constexpr (V <= 3) {
                 double x[1], y[1];
-                if (V == 1)
-                    b1_pairs<1>(wu, wv, p.tp, tab, x, y);
-                else
-                    b2_pairs<1>(wu, wv, p.tp, tab, x, y);
+                if constexpr (V == 3) {
+                    const uint64_t w1[1] = {w[0]}, w2[1] = {w[1]}, w3[1] = {w[per - 1]};
+                    b3_pairs<1>(w1, w2, w3, p.tp, tab, x, y);
+                } else {
+                    const uint64_t wu[1] = {w[0]}, wv[1] = {w[1]};
+                    if (V == 1)
+                        b1_pairs<1>(wu, wv, p.tp, tab, x, y);
+                    else
+                        b2_pairs<1>(wu, wv, p.tp, tab, x, y);
+                }
                 const uint32_t take = qk.cnt - j < 32 ? (uint32_t)(qk.cnt - j) : 32u;
                 if ((uint32_t)lane < take)
                     store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + lane), p.shift, p.n, x[0], y[0], p.aligned);
-                words = 2 * take;
+                words = per * take;
                 j += take;
             } else {
-                PolarCand c[1];
-                const bool ok = polar_candidate(w0, w1, c[0]);
+                bool ok;
                 double x[1], y[1];
-                polar_transform<1>(c, p.tp, tab, x, y);
+                if constexpr (V == 6) {
+                    const uint64_t wu[1] = {w[0]}, wv[1] = {w[1]};
+                    bool okr[1];
+                    ratio_candidates<1>(wu, wv, tab, x, okr);
+                    ok = okr[0];
+                } else {
+                    PolarCand c[1];
+                    ok = polar_candidate(w[0], w[1], c[0]);
+                    if (V == 5)
+                        p2_transform<1>(c, p.tp, tab, x, y);
+                    else
+                        polar_transform<1>(c, p.tp, tab, x, y);
+                }
                 const unsigned m = __ballot_sync(kFull, ok);
                 const uint32_t need = (uint32_t)(qk.cnt - j), rank = __popc(m & lt);
-                if (ok && rank < need)
-                    store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + rank), p.shift, p.n, x[0], y[0], p.aligned);
+                if (ok && rank < need) {
+                    if constexpr (V == 6) {
+                        const uint64_t g = qk.off + j + rank;  // one normal per accepted candidate
+                        if (g < p.n) p.out[g - p.shift] = __fma_rn(p.tp.sigma, x[0], p.tp.mu);
+                    } else {
+                        store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + rank), p.shift, p.n, x[0], y[0], p.aligned);
+                    }
+                }
                 const uint32_t got = __popc(m);
                 if (got >= need) {  // exact stop: nothing after the need-th accept is consumed
                     const unsigned last = __ballot_sync(kFull, ok && rank == need - 1);
@@ -1371,9 +1408,9 @@ __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
                     j += got;
                 }
             }
-            if ((uint32_t)(2 * lane) < words) {  // write back the consumed words in place
-                r[pa] = w0;
-                r[pa1] = w1;
+            if ((uint32_t)(per * lane) < words) {  // write back the consumed words in place
+#pragma unroll
+                for (int t = 0; t < per; ++t) r[pa[t]] = w[t];
             }
             i0 += words;
             __syncwarp();

@@ -434,16 +434,17 @@ def test_wide_multi_block_calls_state_continuity(method):
         assert_state_equal(g, st)
 
 
-@pytest.mark.parametrize("method", ["B1", "B2", "P"])
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P", "P2", "R", "R1"])
 def test_mid_quota_calls(method):
     # per-stream quotas of 12..128 pairs run one warp per stream straight through the HBM ring
     # (mid_kernel): ragged quotas, odd n, partial last steps, consecutive calls, state bit-exact
     S = 512
     g, st = P.Generator(17, S, first_stream=3), O.Streams(17, S, first_stream=3)
+    per = 1 if method in ("R", "R1") else 2  # R's unit is a normal
     for pairs, extra in ((12, 0), (31, 2 * 100 + 1), (33, 2 * 511), (64, 7), (100, 2 * 5), (128, 0), (45, 1)):
-        n = 2 * S * pairs + extra
+        n = per * S * pairs + extra
         d = gen_normals(g, method, n, 0.5, 2.0)
-        o = ora_normals(st, method, n, 0.5, 2.0)
+        o = ora_normals(st, "R" if method == "R1" else method, n, 0.5, 2.0)
         assert d.size == n and np.max(np.abs(d - o)) <= tol_for(method), (method, pairs, extra)
     assert_state_equal(g, st)
 
