@@ -45,7 +45,7 @@ constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
 constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)
 
 struct Occ {
-    int bm[4] = {0, 0, 0, 0}, polar = 0, ratio = 0, ratio1 = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
+    int bm[4] = {0, 0, 0, 0}, pw[3] = {0, 0, 0}, polar = 0, ratio = 0, ratio1 = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
 };
 
 }  // namespace
@@ -109,6 +109,9 @@ bool epoch_fast(const BulkParams& p) {
     return p.aligned && p.log2E >= 7 && p.rem == 0 && p.q % 128 == 0 && p.n == 2 * p.units && p.shift == 0;
 }
 
+#ifndef NRNG_PW_SMALL
+#define NRNG_PW_SMALL 1
+#endif
 template <int V>
 void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
     const bool plain = p.aligned && p.log2E == 0;
@@ -127,6 +130,11 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
     } else {
         if (plain && ns >= (uint32_t)(kPwWarps * h->num_sms)) {
             pw_kernel<V, kPwWarps><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
+            return;
+        }
+        if (NRNG_PW_SMALL && plain) {  // fewer streams than one-block-per-SM slots: 4-warp blocks
+            pw_kernel<V, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.pw[V], h->num_sms),
+                                           kWarpsPerBlock * 32, bm_smem(kWarpsPerBlock), st>>>(p);
             return;
         }
     }
@@ -342,6 +350,8 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(pw_kernel<4, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
     occupancy(b3_kernel<kTriWarps, true>, kTriWarps, tri_smem(kTriWarps));
     h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    h->occ.pw[1] = occupancy(pw_kernel<1, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    h->occ.pw[2] = occupancy(pw_kernel<2, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     occupancy(pw_kernel<7, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
     h->occ.ratio1 = occupancy(pw_kernel<7, kWarpsPerBlock>, kWarpsPerBlock, r1_smem(kWarpsPerBlock));
     occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));
