@@ -164,6 +164,9 @@ void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t 
         pw_kernel<kPw, kPwWarps><<<h->num_sms, kPwWarps * 32, kPw == 5 ? r1_smem(kPwWarps) : bm_smem(kPwWarps), st>>>(p);
     else if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
         polar_kernel<kBigBlockPolar, M><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
+    else if (M == 1 && NRNG_PW_SMALL && p.aligned && p.log2E == 0 && p.q + 1 < (1ull << 31))
+        pw_kernel<4, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.pw[0], h->num_sms), kWarpsPerBlock * 32,
+                                       bm_smem(kWarpsPerBlock), st>>>(p);
     else
         polar_kernel<kWarpsPerBlock, M><<<grid_for(ns, kWarpsPerBlock, h->occ.polar, h->num_sms),
                                           kWarpsPerBlock * 32, polar_smem(kWarpsPerBlock), st>>>(p);
@@ -350,6 +353,7 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(pw_kernel<4, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
     occupancy(b3_kernel<kTriWarps, true>, kTriWarps, tri_smem(kTriWarps));
     h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    h->occ.pw[0] = occupancy(pw_kernel<4, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     h->occ.pw[1] = occupancy(pw_kernel<1, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     h->occ.pw[2] = occupancy(pw_kernel<2, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     occupancy(pw_kernel<7, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
