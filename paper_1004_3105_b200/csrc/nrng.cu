@@ -45,7 +45,7 @@ constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
 constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)
 
 struct Occ {
-    int bm[4] = {0, 0, 0, 0}, pw[3] = {0, 0, 0}, polar = 0, ratio = 0, ratio1 = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
+    int bm[4] = {0, 0, 0, 0}, pw[3] = {0, 0, 0}, tri = 0, polar = 0, ratio = 0, ratio1 = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
 };
 
 }  // namespace
@@ -125,6 +125,11 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
     if constexpr (V == 3) {
         if (plain && ns >= (uint32_t)(kTriWarps * h->num_sms)) {
             b3_kernel<kTriWarps><<<h->num_sms, kTriWarps * 32, tri_smem(kTriWarps), st>>>(p);
+            return;
+        }
+        if (NRNG_PW_SMALL && plain) {  // fewer streams than one-block-per-SM slots: 4-warp blocks
+            b3_kernel<kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.tri, h->num_sms), kWarpsPerBlock * 32,
+                                        tri_smem(kWarpsPerBlock), st>>>(p);
             return;
         }
     } else {
@@ -354,6 +359,7 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(b3_kernel<kTriWarps, true>, kTriWarps, tri_smem(kTriWarps));
     h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     h->occ.pw[0] = occupancy(pw_kernel<4, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    h->occ.tri = occupancy(b3_kernel<kWarpsPerBlock>, kWarpsPerBlock, tri_smem(kWarpsPerBlock));
     h->occ.pw[1] = occupancy(pw_kernel<1, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     h->occ.pw[2] = occupancy(pw_kernel<2, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     occupancy(pw_kernel<7, kPwWarps>, kPwWarps, r1_smem(kPwWarps));

@@ -7,7 +7,7 @@ import paper_1004_3105_b200 as P
 for S, n in ((1024, 1 << 20), (1024, 1 << 22), (2048, 1 << 24)):
     g = P.Generator(1, S)
     out = torch.empty(n, dtype=torch.float64, device='cuda')
-    for m in ("B1", "B2", "P"):
+    for m in ("B1", "B2", "B3", "P"):
         for _ in range(3):
             g.normal(m, out=out)
         s = torch.cuda.Stream()
