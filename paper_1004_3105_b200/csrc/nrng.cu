@@ -150,8 +150,8 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
                                        bm_smem(kWarpsPerBlock), st>>>(p);
 }
 
-#ifndef NRNG_P2_PW  // P2 on pw_kernel<5> (compacted tails, 104 registers): 6.25 ms vs 6.21 on polar_kernel
-#define NRNG_P2_PW 0
+#ifndef NRNG_P2_PW  // P2 on pw_kernel<5> (compacted tails, 104 registers, no mirror): 6.21 vs 6.20 ms burst,
+#define NRNG_P2_PW 1  // 6.24 vs 6.39 ms sustained against polar_kernel
 #endif
 template <int M>
 void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
