@@ -165,6 +165,20 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: re-run this script under torchrun with
+    N ranks (one per GPU, 127.0.0.1 rendezvous); rank 0's JSON line is the output."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def config_block(n_gpus):
     return {"workload": "BASELINE configs[4] per-GPU shard: 2^31 fp64 normals/GPU from 2^16 LFG(607,273) "
                         "streams/GPU (global ids [r*2^16,(r+1)*2^16)), seed 11, mu 0, sigma 1; one call per "
@@ -187,6 +201,8 @@ def main():
     ap.add_argument("--validate", type=int, default=1)
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -251,36 +267,16 @@ def main():
     total_normals = world * len(METHODS) * CFG.n * args.steps
     value = total_normals / (elapsed / 1e3)
 
-    # ---- validation: moments + histogram per method, all-reduced over NCCL (the only exchange)
+    # ---- validation: moments + histograms + serial correlation per method, all-reduced over
+    # NCCL (the only exchange; dist.validate, the same code the gloo test runs on CPU)
     validation = {}
     if args.validate:
-        from statistics import NormalDist
-
         from paper_1004_3105_b200 import dist as D
-        from paper_1004_3105_b200 import gof as G
 
-        K = 256
-        edges = [CFG.mu + CFG.sigma * NormalDist().inv_cdf(i / K) for i in range(1, K)]
         for m in METHODS:
             g.normal(m, out=out, mu=CFG.mu, sigma=CFG.sigma)
-            sums, hist = P.stats(out, CFG.mu, edges)
-            sums, hist = D.allreduce_stats(sums, hist)  # NCCL: the run's only GPU<->GPU exchange
-            fine = P.gof_hist(out, CFG.mu, CFG.sigma, 20)
-            if world > 1:
-                dist.all_reduce(fine)
-            gofr = G.ks_ad(fine.cpu().numpy())
-            lag = torch.from_numpy(P.serial_corr(out, CFG.mu, 100)).to(dev)  # lags 0..100
-            if world > 1:
-                dist.all_reduce(lag)
-            serial = G.serial_corr_gate(lag.cpu().numpy(), world * CFG.n)
-            sums, hist = sums.cpu().numpy(), hist.cpu().numpy()
-            n = world * CFG.n
-            v = D.moments(sums, n, CFG.sigma)
-            v.update({"chi2": D.chi_square(hist, n), "dof": K - 1, "min": float(sums[4]), "max": float(sums[5]),
-                      "ks_d": gofr["ks_d"], "ks_pass": gofr["ks_pass"], "ad_a2": gofr["ad_a2"],
-                      "ad_pass": gofr["ad_pass"], "serial_r_max": serial["serial_r_max"],
-                      "serial_lag_max": serial["serial_lag_max"], "serial_pass": serial["serial_pass"]})
-            validation[m] = v
+            validation[m] = D.validate(out, CFG.n, CFG.mu, CFG.sigma, stats=P.stats, gof_hist=P.gof_hist,
+                                       serial=P.serial_corr, world=world, rank=rank)
 
     # ---- e2e: the same step through the public API with HOST output buffers (pinned),
     # the device->host copies inside the timed region (library chunked/overlapped path)

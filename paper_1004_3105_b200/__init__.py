@@ -242,6 +242,32 @@ def _stream_ptr(torch):
     return torch.cuda.current_stream().cuda_stream
 
 
+def out_buffer(out, device=None):
+    """(pointer, number of doubles) of a caller's output buffer, after checking that the
+    library may write 8 * size bytes there: float64, C-contiguous, and -- for a CUDA tensor --
+    on the handle's device (`device`, a torch.device).  A numpy array or CPU tensor is a host
+    buffer (the library's host-output path).  Raises TypeError / ValueError otherwise."""
+    if isinstance(out, np.ndarray):
+        if out.dtype != np.float64:
+            raise TypeError("out must be float64, got %s" % out.dtype)
+        if not out.flags.c_contiguous or not out.flags.writeable:
+            raise ValueError("out must be a writeable C-contiguous array")
+        return out.ctypes.data, out.size
+    torch = _torch()
+    if not isinstance(out, torch.Tensor):
+        raise TypeError("out must be a torch tensor or a numpy array, got %s" % type(out).__name__)
+    if out.dtype != torch.float64:
+        raise TypeError("out must be float64, got %s" % out.dtype)
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
+    if out.device.type == "cuda":
+        if device is not None and out.device != torch.device(device):
+            raise ValueError("out is on %s but the generator lives on %s" % (out.device, device))
+    elif out.device.type != "cpu":
+        raise ValueError("out must be a CUDA or CPU tensor, got %s" % out.device)
+    return out.data_ptr(), out.numel()
+
+
 class Generator:
     """A set of LFG streams [first_stream, first_stream + n_streams) on the current CUDA device.
 
@@ -276,13 +302,11 @@ class Generator:
             nrng_set_stream(self.h, sp)
             self._stream = sp
 
-    def _out(self, n, out, dtype=None):
-        torch = _torch()
+    def _out(self, n, out):
         if out is None:
-            out = torch.empty(n, dtype=dtype or torch.float64, device=self.device)
-        if isinstance(out, np.ndarray):
-            return out, out.ctypes.data, out.size
-        return out, out.data_ptr(), out.numel()
+            out = _torch().empty(n, dtype=_torch().float64, device=self.device)
+        ptr, size = out_buffer(out, self.device)
+        return out, ptr, size
 
     def normal_boxmuller(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, variant: int = 0, out=None):
         out, ptr, n = self._out(n, out)
@@ -364,10 +388,21 @@ class Generator:
         return nrng_kernel_launches(self.h)
 
 
+def _device_f64(x, what="x"):
+    """A contiguous float64 CUDA tensor for the device-side hooks (raises otherwise)."""
+    torch = _torch()
+    if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 or x.device.type != "cuda":
+        raise TypeError("%s must be a float64 CUDA tensor" % what)
+    if not x.is_contiguous():
+        raise ValueError("%s must be contiguous" % what)
+    return x
+
+
 def transform_from_uniforms(u, method: int, mu: float = 0.0, sigma: float = 1.0):
     """Device transform on given uniforms: method 1/2/3 = B1/B2/B3, 4 = Polar, 5 = P2, 6 = R, 7 = R1.
     Returns (out, mask)."""
     torch = _torch()
+    _device_f64(u, "u")
     per = 3 if method == 3 else 2
     n_pairs = u.numel() // per
     out = torch.empty(2 * n_pairs, dtype=torch.float64, device=u.device)
@@ -381,6 +416,7 @@ def serial_corr(x, center: float, K: int = 100):
     """Device lagged sums S_k = sum_i (x_i - c)(x_{i+k} - c), k = 0..K, summed over blocks in a
     fixed order (numpy float64 array of K+1)."""
     torch = _torch()
+    _device_f64(x)
     n = x.numel()
     nb = nrng_serial_corr_blocks(n)
     part = torch.empty(max(1, nb) * (K + 1), dtype=torch.float64, device=x.device)
@@ -393,6 +429,7 @@ def serial_corr(x, center: float, K: int = 100):
 def stats(x, center: float, edges):
     """Device validation reduction: (sums[6] = sum d, d^2, d^3, d^4, min, max; hist[K] int64)."""
     torch = _torch()
+    _device_f64(x)
     edges = torch.as_tensor(edges, dtype=torch.float64, device=x.device).contiguous()
     K = edges.numel() + 1
     sums = torch.empty(6, dtype=torch.float64, device=x.device)
@@ -405,6 +442,7 @@ def stats(x, center: float, edges):
 def gof_hist(x, mu: float, sigma: float, log2K: int = 20):
     """Device histogram of Phi((x-mu)/sigma) over 2^log2K equal-probability bins (int32 tensor)."""
     torch = _torch()
+    _device_f64(x)
     hist = torch.empty(1 << log2K, dtype=torch.int32, device=x.device)
     nrng_gof_hist(x.data_ptr(), x.numel(), mu, sigma, log2K, hist.data_ptr(), _stream_ptr(torch))
     return hist

@@ -109,6 +109,13 @@ bool epoch_fast(const BulkParams& p) {
     return p.aligned && p.log2E >= 7 && p.rem == 0 && p.q % 128 == 0 && p.n == 2 * p.units && p.shift == 0;
 }
 
+// Largest per-stream unit count of one launch (a piece's, if the call is split).
+uint64_t eff_qmax(const BulkParams& p) {
+    const uint64_t qmax = p.q + (p.rem ? 1 : 0);
+    if (!p.jcap) return qmax;
+    return std::min(qmax > p.jb ? qmax - p.jb : 0, p.jcap);
+}
+
 #ifndef NRNG_PW_SMALL
 #define NRNG_PW_SMALL 1
 #endif
@@ -156,20 +163,20 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
 template <int M>
 void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st) {
     constexpr int kPw = M == 1 ? 4 : 5;  // pw_kernel's P and P2 transforms
-    if (M == 1 && epoch_fast(p) && p.q + 1 < (1ull << 31) && ns >= (uint32_t)(kPwWarps * h->num_sms)) {
+    if (M == 1 && epoch_fast(p) && eff_qmax(p) < (1ull << 31) && ns >= (uint32_t)(kPwWarps * h->num_sms)) {
         pw_kernel<4, kPwWarps, true><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
         return;
     }
-    if (M == 2 && epoch_fast(p) && p.q + 1 < (1ull << 31) && ns >= (uint32_t)(kBigBlockPolar * h->num_sms)) {
+    if (M == 2 && epoch_fast(p) && eff_qmax(p) < (1ull << 31) && ns >= (uint32_t)(kBigBlockPolar * h->num_sms)) {
         polar_kernel<kBigBlockPolar, 2, true><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
         return;
     }
-    if ((M == 1 || NRNG_P2_PW) && p.aligned && p.log2E == 0 && p.q + 1 < (1ull << 31) &&
+    if ((M == 1 || NRNG_P2_PW) && p.aligned && p.log2E == 0 && eff_qmax(p) < (1ull << 31) &&
         ns >= (uint32_t)(kPwWarps * h->num_sms))
         pw_kernel<kPw, kPwWarps><<<h->num_sms, kPwWarps * 32, kPw == 5 ? r1_smem(kPwWarps) : bm_smem(kPwWarps), st>>>(p);
     else if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
         polar_kernel<kBigBlockPolar, M><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
-    else if (M == 1 && NRNG_PW_SMALL && p.aligned && p.log2E == 0 && p.q + 1 < (1ull << 31))
+    else if (M == 1 && NRNG_PW_SMALL && p.aligned && p.log2E == 0 && eff_qmax(p) < (1ull << 31))
         pw_kernel<4, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.pw[0], h->num_sms), kWarpsPerBlock * 32,
                                        bm_smem(kWarpsPerBlock), st>>>(p);
     else
@@ -179,7 +186,7 @@ void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t 
 
 cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st) {
     uint32_t ns = p.s_end - p.s_begin;
-    const uint64_t qmax = p.q + (p.rem ? 1 : 0);
+    const uint64_t qmax = eff_qmax(p);
     if (kind != Kind::UNIFORM && qmax >= kMidMinPairs && qmax <= kMidMaxPairs && NRNG_MID_MAX > 0) {
         const unsigned grid = (unsigned)std::min<uint64_t>((ns + kMidWarps - 1) / kMidWarps, (uint64_t)h->num_sms * 16);
         switch (kind) {
@@ -194,7 +201,7 @@ cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st)
         h->launches += 1;
         return cudaGetLastError();
     }
-    if (kind != Kind::UNIFORM && p.q + (p.rem ? 1 : 0) <= kTinyMaxPairs) {
+    if (kind != Kind::UNIFORM && qmax <= kTinyMaxPairs) {
         const unsigned grid = (ns + kTinyThreads - 1) / kTinyThreads;
         switch (kind) {
             case Kind::BM1: tiny_kernel<1><<<grid, kTinyThreads, 0, st>>>(p); break;
@@ -257,10 +264,19 @@ int ensure_staging(nrng_handle h) {
     return NRNG_OK;
 }
 
-// Fill `n` slots (units = pairs for normals, per_unit = 2; or uniforms, per_unit = 1)
-// into `out` (device or host).  Host outputs are produced stream-range by stream-range
-// into two alternating device staging buffers; each chunk's D2H copy on the copy
-// stream overlaps the next chunk's kernel.
+// Per-stream quotas above this many units run as pieces of at most this many units per
+// stream (BulkParams::jb/jcap): every kernel then counts a stream's units and words of one
+// launch in 32 bits, and host outputs never need more than one staging buffer per stream.
+constexpr uint64_t kPieceUnits = uint64_t(1) << 28;
+
+// Fill `n` slots (units = pairs for normals, per_unit = 2; or uniforms / R's normals,
+// per_unit = 1) into `out` (device or host).
+//  * device output: one launch over all streams; quotas above kPieceUnits per stream run
+//    as consecutive pieces (per-stream partition invariance makes that exact).
+//  * host output: generated into two alternating device staging buffers of kStageDoubles
+//    slots, each chunk's D2H copy on the copy stream overlapping the next chunk's kernel.
+//    A chunk is a range of whole streams; a stream whose slots exceed a staging buffer is
+//    produced alone, in pieces of kStageDoubles / per_unit units.
 int run_bulk(nrng_handle h, Kind kind, double* out, size_t n, uint64_t units, int per_unit, double mu,
              double sigma) {
     BulkParams p{};
@@ -272,44 +288,71 @@ int run_bulk(nrng_handle h, Kind kind, double* out, size_t n, uint64_t units, in
     p.n = n;
     p.tp = TParams{mu, sigma, sigma * 0x1.6a09e667f3bcdp+0};
     const uint32_t active = p.q == 0 ? (uint32_t)p.rem : h->S;  // streams with work
+    const uint64_t qmax = p.q + (p.rem ? 1 : 0);
     if (is_device_pointer(out)) {
         p.out = out;
         p.shift = 0;
         p.aligned = ((uintptr_t)out & 15) == 0;
         p.s_begin = 0;
         p.s_end = active;
-        return cuda_err(launch_bulk(h, kind, p, h->stream));
+        if (qmax <= kPieceUnits) return cuda_err(launch_bulk(h, kind, p, h->stream));
+        p.jcap = kPieceUnits;
+        cudaError_t e = cudaSuccess;
+        for (p.jb = 0; p.jb < qmax && e == cudaSuccess; p.jb += kPieceUnits) e = launch_bulk(h, kind, p, h->stream);
+        return cuda_err(e);
     }
     int rc = ensure_staging(h);
     if (rc != NRNG_OK) return set_err(rc);
-    // streams per chunk so that one chunk's slots fit a staging buffer
-    const uint64_t slots_per_stream = (p.q + 1) * per_unit;
-    const uint64_t g = std::max<uint64_t>(1, kStageDoubles / slots_per_stream);
     auto slot_off = [&](uint64_t k) { return (k * p.q + std::min<uint64_t>(k, p.rem)) * per_unit; };
     int buf = 0;
     cudaError_t e = cudaSuccess;
-    for (uint64_t b = 0; b < active && e == cudaSuccess; b += g, buf ^= 1) {
-        const uint64_t en = std::min<uint64_t>(active, b + g);
-        const uint64_t lo = slot_off(b);
-        const uint64_t hi = std::min<uint64_t>(slot_off(en), n);
-        if (hi <= lo) continue;
+    // one chunk: streams [b, en), units [jb, jb + jcap) of each (jcap = 0: all), slots [lo, hi)
+    auto chunk = [&](uint64_t b, uint64_t en, uint64_t jb, uint64_t jcap, uint64_t lo, uint64_t hi) {
+        if (hi <= lo) return;
+        if (hi - lo > kStageDoubles) {  // cannot happen by construction; never write past a stage
+            e = cudaErrorInvalidValue;
+            return;
+        }
         e = cudaStreamWaitEvent(h->stream, h->ev_free[buf], 0);  // previous copy out of this buffer done
-        if (e != cudaSuccess) break;
+        if (e != cudaSuccess) return;
         p.out = h->stage[buf];
         p.shift = lo;
         p.aligned = 1;
         p.s_begin = (uint32_t)b;
         p.s_end = (uint32_t)en;
+        p.jb = jb;
+        p.jcap = jcap;
         e = launch_bulk(h, kind, p, h->stream);
-        if (e != cudaSuccess) break;
+        if (e != cudaSuccess) return;
         e = cudaEventRecord(h->ev_ready[buf], h->stream);
-        if (e != cudaSuccess) break;
+        if (e != cudaSuccess) return;
         e = cudaStreamWaitEvent(h->copy_stream, h->ev_ready[buf], 0);
-        if (e != cudaSuccess) break;
+        if (e != cudaSuccess) return;
         e = cudaMemcpyAsync(out + lo, h->stage[buf], (hi - lo) * sizeof(double), cudaMemcpyDeviceToHost,
                             h->copy_stream);
-        if (e != cudaSuccess) break;
+        if (e != cudaSuccess) return;
         e = cudaEventRecord(h->ev_free[buf], h->copy_stream);
+        buf ^= 1;
+    };
+    const uint64_t slots_per_stream = qmax * per_unit;
+    if (slots_per_stream <= kStageDoubles) {
+        // whole streams per chunk, as many as fit a staging buffer
+        const uint64_t g = kStageDoubles / slots_per_stream;
+        for (uint64_t b = 0; b < active && e == cudaSuccess; b += g) {
+            const uint64_t en = std::min<uint64_t>(active, b + g);
+            chunk(b, en, 0, 0, slot_off(b), std::min<uint64_t>(slot_off(en), n));
+        }
+    } else {
+        // few streams with long quotas: one stream per chunk, in pieces that fit a stage
+        const uint64_t piece = kStageDoubles / per_unit;
+        for (uint64_t k = 0; k < active && e == cudaSuccess; ++k) {
+            const uint64_t cnt = p.q + (k < p.rem ? 1 : 0);
+            for (uint64_t jb = 0; jb < cnt && e == cudaSuccess; jb += piece) {
+                const uint64_t lo = slot_off(k) + jb * per_unit;
+                const uint64_t hi = std::min<uint64_t>(lo + std::min(piece, cnt - jb) * per_unit, n);
+                chunk(k, k + 1, jb, piece, lo, hi);
+            }
+        }
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(h->copy_stream);
     return cuda_err(e);
@@ -611,7 +654,7 @@ int nrng_stats(const double* dev_x, size_t n, double center, const double* dev_e
     const int nblocks = (int)std::max<uint64_t>(1, std::min<uint64_t>((n + kStatsThreads - 1) / kStatsThreads,
                                                                       (uint64_t)sms * 8));
     double* partial = nullptr;
-    cudaError_t e = cudaMallocAsync(&partial, (size_t)nblocks * 6 * sizeof(double), st);
+    cudaError_t e = cudaMallocAsync(&partial, (size_t)nblocks * kStatsPartial * sizeof(double), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(dev_hist, 0, (size_t)K * sizeof(int64_t), st);
     if (e == cudaSuccess) {
         stats_partial_kernel<<<nblocks, kStatsThreads, 0, st>>>(dev_x, n, center, dev_edges, K, partial,
@@ -701,6 +744,7 @@ int nrng_get_state(nrng_handle h, uint64_t* host_ring, uint64_t* host_counts) {
 
 int nrng_set_state(nrng_handle h, const uint64_t* host_ring, const uint64_t* host_counts) {
     if (!h) return set_err(NRNG_EINVAL);
+    h->seq.len = h->seq.pos = 0;  // deviates buffered by the sequential mode came from the old state
     cudaError_t e = cudaSuccess;
     if (host_ring)
         e = cudaMemcpy2DAsync(h->ring, kPitch * sizeof(uint64_t), host_ring, kLagR * sizeof(uint64_t),

@@ -19,6 +19,9 @@ struct BulkParams {
     uint64_t* count;    // S
     double* out;
     uint64_t units, q, rem, shift, n;
+    // a piece of every stream's quota (host-side splitting of very long per-stream quotas):
+    // units [jb, jb + jcap) of stream k's quota, at their own output slots; jcap = 0: whole quota
+    uint64_t jb, jcap;
     uint32_t s_begin, s_end;
     TParams tp;
     int aligned;
@@ -28,6 +31,16 @@ struct BulkParams {
     // an epoch, so consecutive calls continue one canonical sequence.
     uint32_t log2E, S;
 };
+
+__device__ __forceinline__ Quota quota(const BulkParams& p, uint64_t k) {
+    Quota r = quota(p.q, p.rem, k);
+    if (p.jcap) {
+        const uint64_t left = r.cnt > p.jb ? r.cnt - p.jb : 0;
+        r.cnt = left < p.jcap ? left : p.jcap;
+        r.off += p.jb;
+    }
+    return r;
+}
 
 __device__ __forceinline__ uint64_t pair_slot(const BulkParams& p, uint64_t off, uint32_t k, uint64_t j) {
     if (p.log2E == 0) return off + j;
@@ -155,7 +168,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
-        const Quota qk = quota(p.q, p.rem, k);
+        const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
         prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
@@ -404,7 +417,7 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
     double* const scr = reinterpret_cast<double*>(buf + kTriAlloc);
     const unsigned lt = lanemask_lt(lane);
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
-        const Quota qk = quota(p.q, p.rem, k);
+        const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
         prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
@@ -448,7 +461,7 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         // Re-derive the per-stream values from k (kernel parameters live in the constant
         // bank): nothing but k and `nit` has to stay live across the loop, which kept
         // the compiler from rematerialising the quota inside every iteration.
-        const Quota qk2 = quota(p.q, p.rem, k);
+        const Quota qk2 = quota(p, k);
         for (uint64_t j0 = 128ull * nit; j0 < qk2.cnt; j0 += 32) {  // last rows, partial, unsafe pair
             uint64_t w1[1], w2[1], w3[1];
             gen_tri_rows<1>(buf, ps, lane, w1, w2, w3);
@@ -544,7 +557,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
     const unsigned lt = lanemask_lt(lane);
     double* const scr = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + 32 * warp;  // P2 tails
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
-        const Quota qk = quota(p.q, p.rem, k);
+        const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
         prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
@@ -1016,7 +1029,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     const unsigned lt = lanemask_lt(lane);
     double* const scr = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + 32 * warp;  // M = 5, 7
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
-        const Quota qk = quota(p.q, p.rem, k);
+        const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
         if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
@@ -1208,7 +1221,7 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
     __syncthreads();
     const uint32_t k = p.s_begin + blockIdx.x * kTinyThreads + threadIdx.x;
     if (k >= p.s_end) return;
-    const Quota qk = quota(p.q, p.rem, k);
+    const Quota qk = quota(p, k);
     if (qk.cnt == 0) return;
     const uint64_t C = p.count[k];
     uint64_t* r = p.ring + (uint64_t)k * kPitch;
@@ -1325,7 +1338,7 @@ __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt(lane);
     for (uint32_t k = p.s_begin + blockIdx.x * kMidWarps + warp; k < p.s_end; k += gridDim.x * kMidWarps) {
-        const Quota qk = quota(p.q, p.rem, k);
+        const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
         uint64_t* r = p.ring + (uint64_t)k * kPitch;
@@ -1429,7 +1442,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) uniform_kernel(BulkParams
     L.buf = smem + warp * kWinAlloc;
     for (uint32_t k = p.s_begin + blockIdx.x * kWarpsPerBlock + warp; k < p.s_end;
          k += gridDim.x * kWarpsPerBlock) {
-        const Quota qk = quota(p.q, p.rem, k);
+        const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
@@ -1541,16 +1554,25 @@ __global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs,
 }
 
 // ------------------------------------------------------------------ validation stats
-// Block partials of sum (x-c)^k, k = 1..4, min, max (fp64), and a K-bin histogram
-// (shared-memory int counters -> global u64 atomics).  A second kernel reduces the
-// block partials in a fixed order (deterministic sums).
+// Block partials of sum (x-c)^k, k = 1..4 (fp64, compensated: each sum carries its running
+// rounding error, Neumaier's variant of Kahan summation, through the thread loop, the warp
+// and block reductions and the final pass -- the 2^34-deviate runs add ~2^15 terms per
+// thread), min, max, and a K-bin histogram (shared-memory int counters -> global u64
+// atomics).  A second kernel reduces the block partials in a fixed order (deterministic).
 constexpr int kStatsThreads = 256;
 constexpr int kStatsCells = 2048;  // uniform cells over [edges[0], edges[K-2]] for the bin lookup
+constexpr int kStatsPartial = 10;  // per block: 4 sums, 4 compensations, min, max
+// s + v with the rounding error of the addition accumulated into c (Neumaier).
+__device__ __forceinline__ void comp_add(double& s, double& c, double v) {
+    const double t = __dadd_rn(s, v);
+    c = __dadd_rn(c, fabs(s) >= fabs(v) ? __dadd_rn(__dadd_rn(s, -t), v) : __dadd_rn(__dadd_rn(v, -t), s));
+    s = t;
+}
 __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(const double* __restrict__ x, uint64_t n,
                                                                       double center, const double* __restrict__ edges,
                                                                       int K, double* __restrict__ partial,
                                                                       unsigned long long* __restrict__ hist) {
-    __shared__ double red[6][kStatsThreads / 32];
+    __shared__ double red[kStatsPartial][kStatsThreads / 32];
     __shared__ unsigned int sh[1024];
     __shared__ double se[1023];
     __shared__ unsigned short cell[kStatsCells];  // edges <= the cell's left end (a lower bound)
@@ -1573,15 +1595,16 @@ __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(const doub
         cell[c] = (unsigned short)a;
     }
     __syncthreads();
-    double s1 = 0, s2 = 0, s3 = 0, s4 = 0, mn = __longlong_as_double(0x7ff0000000000000ULL), mx = -mn;
+    double s[4] = {0, 0, 0, 0}, cs[4] = {0, 0, 0, 0};
+    double mn = __longlong_as_double(0x7ff0000000000000ULL), mx = -mn;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const double v = x[i];
-        const double d = v - center;
-        const double d2 = d * d;
-        s1 += d;
-        s2 += d2;
-        s3 += d2 * d;
-        s4 += d2 * d2;
+        const double d = __dadd_rn(v, -center);
+        const double d2 = __dmul_rn(d, d);
+        comp_add(s[0], cs[0], d);
+        comp_add(s[1], cs[1], d2);
+        comp_add(s[2], cs[2], __dmul_rn(d2, d));
+        comp_add(s[3], cs[3], __dmul_rn(d2, d2));
         mn = fmin(mn, v);
         mx = fmax(mx, v);
         int b;
@@ -1599,36 +1622,61 @@ __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(const doub
         atomicAdd(&sh[b], 1u);
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double vals[6] = {s1, s2, s3, s4, mn, mx};
 #pragma unroll
-    for (int t = 0; t < 6; ++t) {
-        double v = vals[t];
+    for (int t = 0; t < 4; ++t) {
         for (int o = 16; o > 0; o >>= 1) {
-            const double w = __shfl_xor_sync(kFull, v, o);
-            v = t < 4 ? v + w : (t == 4 ? fmin(v, w) : fmax(v, w));
+            const double ws = __shfl_xor_sync(kFull, s[t], o), wc = __shfl_xor_sync(kFull, cs[t], o);
+            comp_add(s[t], cs[t], ws);
+            cs[t] = __dadd_rn(cs[t], wc);
         }
-        if (lane == 0) red[t][warp] = v;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
+        mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            red[t][warp] = s[t];
+            red[4 + t][warp] = cs[t];
+        }
+        red[8][warp] = mn;
+        red[9][warp] = mx;
     }
     __syncthreads();
-    if (threadIdx.x < 6) {
+    if (threadIdx.x < 4) {
         const int t = threadIdx.x;
+        double v = red[t][0], c = red[4 + t][0];
+        for (int w = 1; w < kStatsThreads / 32; ++w) {
+            comp_add(v, c, red[t][w]);
+            c = __dadd_rn(c, red[4 + t][w]);
+        }
+        partial[blockIdx.x * kStatsPartial + t] = v;
+        partial[blockIdx.x * kStatsPartial + 4 + t] = c;
+    } else if (threadIdx.x < 6) {
+        const int t = threadIdx.x + 4;  // 8: min, 9: max
         double v = red[t][0];
-        for (int w = 1; w < kStatsThreads / 32; ++w)
-            v = t < 4 ? v + red[t][w] : (t == 4 ? fmin(v, red[t][w]) : fmax(v, red[t][w]));
-        partial[blockIdx.x * 6 + t] = v;
+        for (int w = 1; w < kStatsThreads / 32; ++w) v = t == 8 ? fmin(v, red[t][w]) : fmax(v, red[t][w]);
+        partial[blockIdx.x * kStatsPartial + t] = v;
     }
     for (int b = threadIdx.x; b < K; b += blockDim.x)
         if (sh[b]) atomicAdd(&hist[b], (unsigned long long)sh[b]);
 }
 
+// sums[0..3] = the compensated power sums (sum + accumulated error), sums[4] = min, [5] = max.
 __global__ void stats_final_kernel(const double* __restrict__ partial, int nblocks, double* __restrict__ sums) {
     const int t = threadIdx.x;
-    if (t < 6) {
-        double v = partial[t];
+    if (t < 4) {
+        double v = partial[t], c = partial[4 + t];
         for (int b = 1; b < nblocks; ++b) {
-            const double w = partial[b * 6 + t];
-            v = t < 4 ? v + w : (t == 4 ? fmin(v, w) : fmax(v, w));
+            comp_add(v, c, partial[b * kStatsPartial + t]);
+            c = __dadd_rn(c, partial[b * kStatsPartial + 4 + t]);
         }
+        sums[t] = __dadd_rn(v, c);
+    } else if (t < 6) {
+        double v = partial[4 + t];
+        for (int b = 1; b < nblocks; ++b) v = t == 4 ? fmin(v, partial[b * kStatsPartial + 4 + t])
+                                                     : fmax(v, partial[b * kStatsPartial + 4 + t]);
         sums[t] = v;
     }
 }

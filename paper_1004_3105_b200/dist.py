@@ -54,3 +54,72 @@ def chi_square(hist, n: int) -> float:
     K = len(hist)
     e = n / K
     return float(sum((float(h) - e) ** 2 / e for h in hist))
+
+
+def cross_rank_lag_sums(tail, head_next, lags: int):
+    """Lagged products sum_i d_i d_{i+k}, k = 0..lags, over the pairs (i, i+k) that straddle
+    a rank boundary: i among the last `lags` deviates of rank r (`tail`, centred), i+k among
+    the first `lags` of rank r+1 (`head_next`, centred).  k = 0 has none."""
+    import numpy as np
+
+    t = np.asarray(tail, np.float64)
+    h = np.asarray(head_next, np.float64)
+    out = np.zeros(lags + 1)
+    L = t.size
+    for k in range(1, lags + 1):
+        # i = L - a (a = 1..min(k, L)) pairs with head index k - a
+        a = np.arange(1, min(k, L) + 1)
+        a = a[k - a < h.size]
+        out[k] = float(np.dot(t[L - a], h[k - a]))
+    return out
+
+
+def validate(x, n_local: int, mu: float, sigma: float, *, stats, gof_hist, serial, world: int = 1,
+             rank: int = 0, K: int = 256, log2K: int = 20, lags: int = 100, group=None) -> dict:
+    """The bench's validation of one method's output, identical on every rank count: each
+    rank's deviates `x` are the contiguous slice [rank n_local, (rank+1) n_local) of the
+    global stream-major output (Q6), so the gates see the whole 2^34-deviate sequence.
+      * moments + K-bin chi-square: per-rank power sums / histogram (`stats`), all-reduced;
+      * KS / Anderson-Darling: per-rank 2^log2K-bin probability histogram (`gof_hist`), summed;
+      * serial correlation, lags 1..`lags`: per-rank lagged sums (`serial`) plus the products
+        that straddle each rank boundary (first `lags` deviates all-gathered), summed.
+    `stats(x, center, edges) -> (sums[6], hist[K])` tensors, `gof_hist(x, mu, sigma, log2K)`
+    -> int tensor, `serial(x, center, lags)` -> numpy (lags + 1) -- the device kernels in
+    bench.py, CPU stand-ins in the gloo test.  The only exchanges are these reductions."""
+    from statistics import NormalDist
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from . import gof as G
+
+    multi = world > 1 and dist.is_available() and dist.is_initialized()
+    edges = [mu + sigma * NormalDist().inv_cdf(i / K) for i in range(1, K)]
+    sums, hist = stats(x, mu, edges)
+    sums, hist = allreduce_stats(sums, hist, group=group)
+    fine = gof_hist(x, mu, sigma, log2K).to(torch.int64)
+    if multi:
+        dist.all_reduce(fine, group=group)
+    gofr = G.ks_ad(fine.cpu().numpy())
+    lag = np.asarray(serial(x, mu, lags), np.float64)
+    if multi:
+        m = min(lags, n_local)
+        head = (x[:m].to(torch.float64) - mu).contiguous()
+        heads = [torch.empty_like(head) for _ in range(world)]
+        dist.all_gather(heads, head, group=group)
+        if rank + 1 < world:
+            tail = (x[n_local - m:].to(torch.float64) - mu).cpu().numpy()
+            lag = lag + cross_rank_lag_sums(tail, heads[rank + 1].cpu().numpy(), lags)
+        lt = torch.from_numpy(lag).to(x.device)
+        dist.all_reduce(lt, group=group)
+        lag = lt.cpu().numpy()
+    n = world * n_local
+    serial_r = G.serial_corr_gate(lag, n)
+    sums, hist = sums.cpu().numpy(), hist.cpu().numpy()
+    v = moments(sums, n, sigma)
+    v.update({"chi2": chi_square(hist, n), "dof": K - 1, "min": float(sums[4]), "max": float(sums[5]),
+              "ks_d": gofr["ks_d"], "ks_pass": gofr["ks_pass"], "ad_a2": gofr["ad_a2"], "ad_pass": gofr["ad_pass"],
+              "serial_r_max": serial_r["serial_r_max"], "serial_lag_max": serial_r["serial_lag_max"],
+              "serial_pass": serial_r["serial_pass"]})
+    return v

@@ -78,3 +78,31 @@ def test_no_cpu_fallback_in_product_package():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "liboracle" not in src, f
+
+
+def test_output_buffer_checks():
+    # the binding refuses buffers the library would overrun: wrong dtype,
+    # non-contiguous views, read-only arrays; it accepts float64 host arrays / CPU tensors
+    import numpy as np
+    import torch
+
+    import paper_1004_3105_b200 as P
+
+    a = np.empty(10)
+    assert P.out_buffer(a) == (a.ctypes.data, 10)
+    t = torch.empty(7, dtype=torch.float64)
+    assert P.out_buffer(t) == (t.data_ptr(), 7)
+    with pytest.raises(TypeError):
+        P.out_buffer(np.empty(10, np.float32))
+    with pytest.raises(TypeError):
+        P.out_buffer(torch.empty(10, dtype=torch.float32))
+    with pytest.raises(ValueError):
+        P.out_buffer(np.empty(20)[::2])
+    with pytest.raises(ValueError):
+        P.out_buffer(torch.empty(20, dtype=torch.float64)[::2])
+    ro = np.empty(4)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        P.out_buffer(ro)
+    with pytest.raises(TypeError):
+        P.out_buffer([0.0] * 4)

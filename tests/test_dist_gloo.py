@@ -83,3 +83,77 @@ def test_moments_and_gates():
     assert not bad["moments_4se_pass"]
     flat = D.chi_square([100] * 6, 600)
     assert flat == 0.0 and D.chi_square([200, 0, 100, 100, 100, 100], 600) > 100
+
+
+# ---------------------------------------------------------------- bench.py's validation leg
+# dist.validate is what bench.py runs after its timed region (over NCCL); here the same code
+# runs over gloo with CPU stand-ins for the three device reductions, and world size 2 must
+# give the single-process result on the concatenated output (including the lagged products
+# that straddle the rank boundary).
+
+def _cpu_stats(x, center, edges):
+    sums, hist = O.stats(x.numpy(), center, np.asarray(edges))
+    return torch.tensor(sums, dtype=torch.float64), torch.tensor(hist, dtype=torch.int64)
+
+
+def _cpu_gof_hist(x, mu, sigma, log2K):
+    from scipy.stats import norm
+
+    K = 1 << log2K
+    b = np.minimum((norm.cdf((x.numpy() - mu) / sigma) * K).astype(np.int64), K - 1)
+    return torch.from_numpy(np.bincount(b, minlength=K))
+
+
+def _cpu_serial(x, center, lags):
+    d = x.numpy() - center
+    return np.array([np.dot(d[: d.size - k], d[k:]) for k in range(lags + 1)])
+
+
+def _validate_worker(rank, world, port, per_rank, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    st = O.Streams(11, 64, first_stream=64 * rank)
+    x = torch.from_numpy(st.normal_polar(per_rank, 0.0, 1.0))
+    v = D.validate(x, per_rank, 0.0, 1.0, stats=_cpu_stats, gof_hist=_cpu_gof_hist, serial=_cpu_serial,
+                   world=world, rank=rank, log2K=12, lags=100)
+    if rank == 0:
+        q.put(v)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_validate_world2_equals_single_process():
+    world, per_rank = 2, 64 * 2 * 1000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_validate_worker, args=(r, world, port, per_rank, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    v2 = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    full = torch.from_numpy(O.Streams(11, 128).normal_polar(world * per_rank, 0.0, 1.0))
+    v1 = D.validate(full, world * per_rank, 0.0, 1.0, stats=_cpu_stats, gof_hist=_cpu_gof_hist,
+                    serial=_cpu_serial, log2K=12, lags=100)
+    for key in ("mean", "var", "skew", "exkurt", "chi2", "ks_d", "ad_a2", "serial_r_max"):
+        assert math.isclose(v1[key], v2[key], rel_tol=1e-9, abs_tol=1e-15), key
+    for key in ("min", "max", "serial_lag_max", "ks_pass", "ad_pass", "serial_pass", "moments_4se_pass"):
+        assert v1[key] == v2[key], key
+
+
+def test_cross_rank_lag_sums_brute_force():
+    rng = np.random.default_rng(1)
+    a, b = rng.standard_normal(37), rng.standard_normal(50)
+
+    def lagsum(v, k):
+        return float(np.dot(v[: v.size - k], v[k:])) if k < v.size else 0.0
+
+    for lags in (1, 5, 36, 40):
+        ab = np.concatenate([a, b])
+        full = np.array([lagsum(ab, k) for k in range(lags + 1)])
+        sep = np.array([lagsum(a, k) + lagsum(b, k) for k in range(lags + 1)])
+        m = min(lags, 37)
+        cross = D.cross_rank_lag_sums(a[a.size - m:], b[:lags], lags)
+        assert np.allclose(sep + cross, full, rtol=1e-13, atol=1e-12)

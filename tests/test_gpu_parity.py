@@ -2,8 +2,11 @@
 
 Bars (BASELINE.json north_star): uniforms, Polar accept masks, output order, per-stream
 consumption counters and the generator state bit-exact; B1/P normals within 1e-13
-absolute; B2/B3 within 1e-13 + the paper's 1e-10 bound (reading R17) -- and
-B2's sincos16 and B3's bulk branch are in fact bit-exact given identical coefficients.
+absolute.  North star allows B2/B3 1e-13 + the paper's 1e-10 bound (reading
+R17), but both sides evaluate the same approximations with identical coefficients and
+operation order (B2's sincos16 and B3's bulk branch are bit-exact; only ln in B2's radius
+and B3's tail differs by ulps), so B2/B3/P2 are held to the same 1e-13: a regression in
+the coefficients or the doubling at the 1e-11 level fails.
 """
 import math
 
@@ -18,7 +21,7 @@ import paper_1004_3105_b200 as P  # noqa: E402
 from paper_1004_3105_b200 import workloads as W  # noqa: E402
 
 TOL = 1e-13
-TOL_APPROX = 1e-13 + 1e-10
+TOL_APPROX = 1e-13  # B2/B3/P2: same bar as B1/P (see the module docstring)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -566,6 +569,14 @@ def test_stats_histogram_bins_exact(K):
     sums, _ = P.stats(torch.from_numpy(xm).cuda(), 0.25, edges)
     d, s = xm - 0.25, host(sums)
     assert np.allclose(s[:4], [d.sum(), (d ** 2).sum(), (d ** 3).sum(), (d ** 4).sum()], rtol=1e-9, atol=1e-6)
+
+
+def test_stats_sums_are_compensated():
+    # (1e16, 1, -1e16) repeated: every 1 is lost to rounding in a plain fp64 running sum, while
+    # the compensated sums (Neumaier) recover sum d = number of ones
+    x = np.tile([1e16, 1.0, -1e16], 100003)
+    sums, _ = P.stats(torch.from_numpy(x).cuda(), 0.0, [-1.0, 0.0, 1.0])
+    assert abs(host(sums)[0] - 100003) < 1e-3
 
 
 def test_stats_kernel_matches_oracle_stats():
