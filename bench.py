@@ -33,17 +33,20 @@ METRIC = "fp64 normals/sec per method (B1, B3, Polar) at 1/2/4/8 B200; % of roof
 METHODS = ("B1", "B2", "B3", "P")
 CFG = W.C5_SHARD
 BYTES_PER_NORMAL = 8  # algorithmic HBM traffic: one fp64 written per normal
-# Algorithmic FP64 work per pair ("roofline"): the paper's operation sequence
-# for each method, priced with the DP-pipe cost of the cheapest double-accurate primitives
-# we have (table ln 8, radius from ln by one third-order rsqrt step 7, sin+cos of an exactly
-# reduced angle 14, IEEE divide 8, sincos16 of P:162-170 21, Horner-15 15; MUFU seeds and
-# integer work not counted):
+# Algorithmic FP64 work per NORMAL, SURVEY.md §8(d) (the contract): the paper's operation tallies
+# priced with CUDA libdevice fast-path DP-instruction costs.
+W_SURVEY = {"B1": 34.5, "B2": 33.0, "B3": 30.5, "P": 28.5}
+# The same tallies priced with this repo's own double-accurate primitives (table
+# ln 8, radius from ln by one third-order rsqrt step 7, sin+cos of an exactly reduced angle 14,
+# IEEE divide 8, sincos16 of P:162-170 21, Horner-15 15; MUFU seeds and integer work not
+# counted), per PAIR:
 #   B1 = ln + radius + sincos + 2 outputs                                   = 31
 #   B2 = ln + radius + sincos16 + 2                                         = 38
 #   B3 = bulk pair (m^2 1, Moebius 2, div 8, Horner 15, r 2, A 1, sincos16 21, 2) 52;
 #        tail pair (1/9): 1 - m^2 1 + ln 8 + rsqrt 5 + r 2 replace 27 of it  = 52 - 11/9
 #   P  = (4/pi) candidates x 3 (s) + per accepted pair ln 8 + hs 1 + rsqrt 5 + r 2 + 2 = 12/pi + 18
 DP_PER_PAIR = {"B1": 31.0, "B2": 38.0, "B3": 52.0 - 11.0 / 9.0, "P": 12.0 / math.pi + 18.0}
+KERNEL = {"B1": "pw_kernel<1,16>", "B2": "pw_kernel<2,16>", "B3": "b3_kernel<16>", "P": "pw_kernel<4,16>"}
 FP64_PEAK_NOMINAL = 148 * 64 * 1.965e9  # SMs x FP64 lanes per SM x max SM clock = DP instr/s
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
 # capture of the same launch (profiles/); None until captured.
@@ -53,6 +56,17 @@ try:
         TRAFFIC = json.load(_fh)
 except Exception:
     pass
+# FP64 DFMA rate and HBM write bandwidth measured on this pool (tools/probe/peaks.cu: burst and
+# sustained under the power cap); MEASURED_PEAKS.json (driver-written) has neither.
+PROBE_PEAKS_FILE = os.path.join(ROOT, "profiles", "peaks.json")
+
+
+def load_probe_peaks():
+    try:
+        with open(PROBE_PEAKS_FILE) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
 
 
 def load_peaks():
@@ -165,6 +179,63 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+def time_configs(P, torch, big, hbm_gbs, fp64_peak, sweep_calls=1000):
+    """BASELINE.json configs[0..3] on this GPU, each at its own shape (one call = one batch):
+    C1 B1, C2 P, C3 B2/B3, and the C4 call-length sweep (B1, P; `sweep_calls` back-to-back calls
+    per length, plain and inside one CUDA graph).  Per entry: us per call, normals/s and the
+    fraction of the floors -- HBM write (8 B/normal), the same plus the generator state read and
+    written back (floor ii: 2 x 4864 B per active stream), and FP64 under SURVEY 8(d)'s W."""
+    res = {}
+    stream = torch.cuda.current_stream()
+
+    def timed(g, m, n, mu, sigma, calls, graph=False):
+        for _ in range(3):
+            g.normal(m, out=big[:n], mu=mu, sigma=sigma)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if graph:
+            gr, s2 = torch.cuda.CUDAGraph(), torch.cuda.Stream()
+            s2.wait_stream(stream)
+            with torch.cuda.stream(s2):
+                with torch.cuda.graph(gr, stream=s2):
+                    for _ in range(calls):
+                        g.normal(m, out=big[:n], mu=mu, sigma=sigma)
+            stream.wait_stream(s2)
+            torch.cuda.synchronize()
+            a.record(stream)
+            gr.replay()
+            b.record(stream)
+        else:
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(calls):
+                g.normal(m, out=big[:n], mu=mu, sigma=sigma)
+            b.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) / calls / 1e3
+        active = min(g.S, (n + 1) // 2)
+        f_hbm = 8 * n / (hbm_gbs * 1e9)
+        f_ii = (8 * n + 2 * 4864 * active) / (hbm_gbs * 1e9)
+        f_w = W_SURVEY[m] * n / fp64_peak
+        return {"n": n, "streams": g.S, "calls": calls, "us_per_call": t * 1e6, "normals_per_s": n / t,
+                "frac_hbm": f_hbm / t, "frac_floor_ii": f_ii / t, "frac_fp64_survey": f_w / t,
+                "frac_roofline_i": max(f_hbm, f_w) / t, "graph": graph}
+
+    for c in (W.C1, W.C2, W.C3):
+        g = P.Generator(c.seed, c.streams)
+        for m in c.methods:
+            res["%s_%s" % (c.name, m)] = timed(g, m, c.n, c.mu, c.sigma, 20)
+        g.close()
+    c = W.C4
+    g = P.Generator(c.seed, c.streams)
+    for m in c.methods:
+        for L in W.C4_LENGTHS:
+            res["C4_%s_n%d" % (m, L)] = timed(g, m, L, c.mu, c.sigma, sweep_calls)
+            if L <= (1 << 18):
+                res["C4_%s_n%d_graph" % (m, L)] = timed(g, m, L, c.mu, c.sigma, sweep_calls, graph=True)
+    g.close()
+    return res
+
+
 def relaunch(n: int) -> int:
     """`python bench.py --gpus N` without a launcher: re-run this script under torchrun with
     N ranks (one per GPU, 127.0.0.1 rendezvous); rank 0's JSON line is the output."""
@@ -199,6 +270,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-streams", type=int, default=4096)
     ap.add_argument("--validate", type=int, default=1)
+    ap.add_argument("--configs", type=int, default=1, help="also time BASELINE configs[0..3] (N=1 only)")
     args = ap.parse_args()
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
@@ -278,6 +350,13 @@ def main():
             validation[m] = D.validate(out, CFG.n, CFG.mu, CFG.sigma, stats=P.stats, gof_hist=P.gof_hist,
                                        serial=P.serial_corr, world=world, rank=rank)
 
+    # ---- BASELINE configs[0..3] at their own shapes (one GPU; the N>1 runs carry the shard step only)
+    configs = None
+    if args.configs and world == 1:
+        pk = load_probe_peaks()
+        configs = time_configs(P, torch, out, pk["hbm_write_gbs_sustained"] if pk else load_peaks()[0]["hbm_gbs"],
+                               pk["fp64_dfma_per_s_sustained"] if pk else FP64_PEAK_NOMINAL)
+
     # ---- e2e: the same step through the public API with HOST output buffers (pinned),
     # the device->host copies inside the timed region (library chunked/overlapped path)
     e2e = None
@@ -324,25 +403,47 @@ def main():
         return
 
     peaks, peak_kind = load_peaks()
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    fp64_peak = FP64_PEAK_NOMINAL
-    roofs = {}
+    hbm_copy = float(peaks.get("hbm_gbs", 6650.0))
+    probe = load_probe_peaks()
+    if probe:
+        fp64_sus, fp64_burst = probe["fp64_dfma_per_s_sustained"], probe["fp64_dfma_per_s_burst"]
+        hbm_w = probe["hbm_write_gbs_sustained"]
+        fp64_src = "measured sustained (%s; burst %.4g)" % (os.path.relpath(PROBE_PEAKS_FILE, ROOT), fp64_burst)
+        hbm_src = "measured write-only sustained (%s); MEASURED_PEAKS.json copy %.1f GB/s" % (
+            os.path.relpath(PROBE_PEAKS_FILE, ROOT), hbm_copy)
+    else:
+        fp64_sus = fp64_burst = FP64_PEAK_NOMINAL
+        hbm_w = hbm_copy
+        fp64_src = "nominal 148 SMs x 64 FP64 lanes x 1965 MHz (no probe file)"
+        hbm_src = peak_kind + " copy (MEASURED_PEAKS.json hbm_gbs)"
+    # per method: the three floors -- HBM write (8 B/normal), FP64 under SURVEY §8(d)'s W, FP64
+    # under the repo's primitive costs -- and the fraction of each; `bound_*` names the floor
+    # that binds under each accounting
+    per_method = {}
     for m in METHODS:
         t = per_ms[m] / 1e3
-        t_hbm = BYTES_PER_NORMAL * CFG.n / (hbm_peak * 1e9)
-        t_alu = DP_PER_PAIR[m] * CFG.n / 2 / fp64_peak
-        if t_alu > t_hbm:
-            roofs[m] = {"bound": "alu", "achieved": DP_PER_PAIR[m] * CFG.n / 2 / t / 1e12, "peak": fp64_peak / 1e12,
-                        "unit": "T DP-instr/s", "frac": t_alu / t,
-                        "peak_source": "derived: 148 SMs x 64 FP64 lanes x 1965 MHz (probe: DFMA 17.09 T/s measured)"}
-        else:
-            roofs[m] = {"bound": "hbm", "achieved": BYTES_PER_NORMAL * CFG.n / t / 1e9, "peak": hbm_peak,
-                        "unit": "GB/s", "frac": t_hbm / t, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)"}
-        roofs[m]["traffic"] = None
+        t_hbm = BYTES_PER_NORMAL * CFG.n / (hbm_w * 1e9)
+        t_w = W_SURVEY[m] * CFG.n / fp64_sus
+        t_r = DP_PER_PAIR[m] * CFG.n / 2 / fp64_sus
+        per_method[m] = {
+            "normals_per_s": world * CFG.n / t, "ms_per_call": per_ms[m], "kernel": KERNEL[m],
+            "hbm_write_gbs": BYTES_PER_NORMAL * CFG.n / t / 1e9,
+            "frac_hbm": t_hbm / t, "frac_fp64_survey": t_w / t, "frac_fp64_repo": t_r / t,
+            "bound_survey": "fp64" if t_w > t_hbm else "hbm", "frac_survey": max(t_w, t_hbm) / t,
+            "bound_repo": "fp64" if t_r > t_hbm else "hbm", "frac_repo": max(t_r, t_hbm) / t,
+            "dp_instr_per_normal_survey": W_SURVEY[m], "dp_instr_per_normal_repo": DP_PER_PAIR[m] / 2,
+        }
     dom = max(METHODS, key=lambda m: per_ms[m])
-    kname = {"B1": "pw_kernel<1,16>", "B2": "pw_kernel<2,16>", "B3": "b3_kernel<16>", "P": "pw_kernel<4,16>"}[dom]
-    roof = dict(roofs[dom], kernel="%s (%s)" % (kname, dom), method=dom)
-    roof["traffic"] = TRAFFIC.get(dom)
+    t = per_ms[dom] / 1e3
+    # the dominant kernel under SURVEY §8(d) (the contract): FP64-bound for every method there
+    roof = {"bound": "alu", "achieved": W_SURVEY[dom] * CFG.n / t / 1e12, "peak": fp64_sus / 1e12,
+            "unit": "T DP-instr/s", "frac": W_SURVEY[dom] * CFG.n / fp64_sus / t,
+            "peak_source": fp64_src, "work": "SURVEY 8(d) W_%s = %.1f DP instr/normal x %d normals per launch"
+            % (dom, W_SURVEY[dom], CFG.n),
+            "frac_repo_accounting": per_method[dom]["frac_repo"], "bound_repo_accounting": per_method[dom]["bound_repo"],
+            "frac_burst_peak": W_SURVEY[dom] * CFG.n / fp64_burst / t,
+            "hbm_peak_gbs": hbm_w, "hbm_peak_source": hbm_src,
+            "kernel": "%s (%s)" % (KERNEL[dom], dom), "method": dom, "traffic": TRAFFIC.get(dom)}
 
     cpu = None
     if not args.no_cpu:
@@ -352,21 +453,23 @@ def main():
         ns = int(min(CFG.streams, max(256, 256 * 10.0 / max(csecs, 1e-3))))
         ns = min(CFG.streams, 1 << int(round(math.log2(ns))))
         cv, cper, cn, csecs = oracle_sample(ns, threads)
+        # and once on a single thread: 16 streams x 2^14 pairs per method
+        v1, cper1, cn1, csecs1 = oracle_sample(16, 1)
         cpu = {"value": cv, "unit": "normals/s", "cores": threads, "kind": "oracle",
                "sample": "%d streams x 2^14 pairs per method (B1,B2,B3,P) = %d normals per method, %.1f s wall"
                          % (ns, cn, csecs),
-               "per_method": cper, "cpu": cpu_model()}
+               "per_method": cper, "cpu": cpu_model(),
+               "single_thread": {"value": v1, "unit": "normals/s", "cores": 1, "per_method": cper1,
+                                 "sample": "16 streams x 2^14 pairs per method = %d normals per method, %.1f s wall"
+                                           % (cn1, csecs1)}}
 
     line = {
         "metric": METRIC, "value": value, "unit": "normals/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_block(world),
-        "per_method": {m: {"normals_per_s": world * CFG.n / (per_ms[m] / 1e3), "ms_per_call": per_ms[m],
-                           "roofline_bound": roofs[m]["bound"], "roofline_frac": roofs[m]["frac"],
-                           "hbm_write_gbs": BYTES_PER_NORMAL * CFG.n / (per_ms[m] / 1e3) / 1e9}
-                       for m in METHODS},
+        "per_method": per_method,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-        "create_s": create_s, "validation": validation,
+        "create_s": create_s, "validation": validation, "configs": configs,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
