@@ -183,8 +183,8 @@ def time_configs(P, torch, big, hbm_gbs, fp64_peak, sweep_calls=1000):
     """BASELINE.json configs[0..3] on this GPU, each at its own shape (one call = one batch):
     C1 B1, C2 P, C3 B2/B3, and the C4 call-length sweep (B1, P; `sweep_calls` back-to-back calls
     per length, plain and inside one CUDA graph).  Per entry: us per call, normals/s and the
-    fraction of the floors -- HBM write (8 B/normal), the same plus the generator state read and
-    written back (floor ii: 2 x 4864 B per active stream), and FP64 under SURVEY 8(d)'s W."""
+    fraction of the floors -- HBM write (8 B/normal), the same plus the generator state the call
+    must read and write back (floor ii), and FP64 under SURVEY 8(d)'s W."""
     res = {}
     stream = torch.cuda.current_stream()
 
@@ -213,8 +213,13 @@ def time_configs(P, torch, big, hbm_gbs, fp64_peak, sweep_calls=1000):
         torch.cuda.synchronize()
         t = a.elapsed_time(b) / calls / 1e3
         active = min(g.S, (n + 1) // 2)
+        # minimal generator-state traffic per active stream: the 2 source words of each of the
+        # w words it generates (at most the 607-word state) read, the last min(w, 607) written back,
+        # the 8-byte counter read and written (sector granularity ignored: a lower bound)
+        w = (2 if m != "B3" else 3) * ((n + 1) // 2 + g.S - 1) // g.S * (1.3 if m == "P" else 1.0)
+        state = active * (8 * min(2 * w, 607) + 8 * min(w, 607) + 16)
         f_hbm = 8 * n / (hbm_gbs * 1e9)
-        f_ii = (8 * n + 2 * 4864 * active) / (hbm_gbs * 1e9)
+        f_ii = (8 * n + state) / (hbm_gbs * 1e9)
         f_w = W_SURVEY[m] * n / fp64_peak
         return {"n": n, "streams": g.S, "calls": calls, "us_per_call": t * 1e6, "normals_per_s": n / t,
                 "frac_hbm": f_hbm / t, "frac_floor_ii": f_ii / t, "frac_fp64_survey": f_w / t,

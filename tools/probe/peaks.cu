@@ -113,10 +113,10 @@ int main() {
     const double w_sus = bytes / (median_of_last(ws, 3.0, 1.0) * 1e-3);
     printf("{\"device\": \"%s\", \"sms\": %d, \"fp64_dfma_per_s_burst\": %.6e, \"fp64_dfma_per_s_sustained\": %.6e, "
            "\"hbm_write_gbs_burst\": %.1f, \"hbm_write_gbs_sustained\": %.1f, \"dfma_launches\": %zu, "
-           "\"store_launches\": %zu, \"how\": \"dfma_loop: %d blocks x %d threads x 8 chains, %d DFMA per launch; "
+           "\"store_launches\": %zu, \"how\": \"dfma_loop: %d blocks x %d threads x 8 chains, %.0f DFMA per launch; "
            "store_kernel: 16-byte st.global.cs over 16 GiB; burst = best of 3 launches from idle, sustained = median "
            "launch of the last 1 s of 3 s back to back\"}\n",
            p.name, p.multiProcessorCount, f_burst, f_sus, w_burst * 1e-9, w_sus * 1e-9, sus.size(), ws.size(), grid,
-           threads, (int)dfma_per_launch);
+           threads, dfma_per_launch);
     return 0;
 }
