@@ -403,7 +403,9 @@ __device__ __forceinline__ void b3_iter(uint64_t* lb, const TParams& tp, const T
     b3_pairs_compact<4>(w1, w2, w3, tp, tab, scr, lane, lt, x, y);
 #pragma unroll
     for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
-    __syncwarp();
+#if !NRNG_SCR_SYNC_MIN
+    __syncwarp();  // (with NRNG_SCR_SYNC_MIN the gather's __syncwarp, after every window access of
+#endif             // this iteration, orders them before the next iteration's window writes)
 }
 
 // Aligned, plain-layout B3 calls (the dispatcher sends the rest to bm_kernel<3>).
@@ -509,6 +511,9 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
 #define NRNG_POLAR_U 4
 #endif
 constexpr int kPU = NRNG_POLAR_U;  // candidates per lane per step (32 kPU per warp)
+#ifndef NRNG_POLAR_SPLIT_STOP
+#define NRNG_POLAR_SPLIT_STOP 1  // pw_polar_block: the exact-stop trim only in the stream's last step
+#endif
 constexpr int kPB = 128; // refill batch: lookahead 64 kPU - 1 + kPB <= 417
 static_assert(64 * kPU - 1 + kPB <= kWin - kLagR && 64 * kPU <= kMirror, "polar window bounds");
 
@@ -915,27 +920,36 @@ __device__ __forceinline__ void pw_bm_block(const PwPtrs& pp, const TParams& tp,
     __syncwarp();
 }
 
-// One Polar step (128 candidates, one block) at compile-time base K; returns whether the
-// quota was reached (exact stop: `used` = candidates consumed of this block).
-template <int M, int K, bool EP = false>
-__device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& tp, const Tables& tab,
-                                               const BulkParams& p, const Quota& qk, double2* o, bool direct,
-                                               uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt,
-                                               double* scr, uint32_t k = 0) {
-    uint64_t wa[kPU], wb[kPU];
-    pw_gen_c<kPU, K>(pp, wa, wb);
-    PolarCand c[kPU];
-    bool ok[kPU];
-    unsigned m[kPU];
+// The accepts of one step trimmed to the remaining quota `need` (exact stop, R5): m[u] keeps
+// only the first `need` accepts in candidate order; returns the candidates consumed.  Called
+// only for the step that reaches the quota (tot >= need).
+__device__ __forceinline__ uint32_t polar_trim(const bool (&ok)[kPU], unsigned (&m)[kPU], uint32_t need,
+                                               unsigned lt) {
+    uint32_t used = 32 * kPU, rem = need;
 #pragma unroll
-    for (int u = 0; u < kPU; ++u) ok[u] = polar_candidate(wa[u], wb[u], c[u]);
-    bool stop;
-    used = polar_rank(ok, m, cnt - acc, lt, stop);
-    double ox[kPU], oy[kPU];
-    if constexpr (M == 5)
-        p2_transform_compact<kPU>(c, ok, tp, tab, scr, lane, lt, ox, oy);
-    else
-        polar_transform<kPU>(c, tp, tab, ox, oy);
+    for (int u = 0; u < kPU; ++u) {
+        const uint32_t nu = __popc(m[u]);
+        if (rem == 0) {
+            m[u] = 0;
+        } else if (nu >= rem) {
+            const unsigned last = __ballot_sync(kFull, ok[u] && (uint32_t)__popc(m[u] & lt) == rem - 1);
+            const int l = __ffs(last) - 1;
+            m[u] &= (l == 31) ? kFull : ((2u << l) - 1u);
+            used = 32 * u + l + 1;
+            rem = 0;
+        } else {
+            rem -= nu;
+        }
+    }
+    return used;
+}
+
+// Stores of one Polar step: accepted candidate i (mask bit) -> output pair acc + its rank.
+template <bool EP>
+__device__ __forceinline__ void pw_polar_stores(const unsigned (&m)[kPU], const double (&ox)[kPU],
+                                                const double (&oy)[kPU], const BulkParams& p, const Quota& qk,
+                                                double2* o, bool direct, uint32_t& acc, int lane, unsigned lt,
+                                                uint32_t k) {
     if (EP) {  // the sequential mode's epoch layout (whole epochs: every pair is in range)
         // a step's <= 128 pairs span at most two epoch chunks of E >= 128 pairs: pair j goes to
         // chunk e0's start + (j - e0 E), plus the jump to the next chunk once j - e0 E >= E
@@ -962,6 +976,52 @@ __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& 
             acc += __popc(m[u]);
         }
     }
+}
+
+// One Polar step (128 candidates, one block) at compile-time base K; returns whether the
+// quota was reached (exact stop: `used` = candidates consumed of this block).  The steady
+// path (the step does not reach the quota: every step of a stream but its last) touches no
+// mask after the ballots; the trim runs only in the last step.
+template <int M, int K, bool EP = false>
+__device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& tp, const Tables& tab,
+                                               const BulkParams& p, const Quota& qk, double2* o, bool direct,
+                                               uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt,
+                                               double* scr, uint32_t k = 0) {
+    uint64_t wa[kPU], wb[kPU];
+    pw_gen_c<kPU, K>(pp, wa, wb);
+    PolarCand c[kPU];
+    bool ok[kPU];
+    unsigned m[kPU];
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) ok[u] = polar_candidate(wa[u], wb[u], c[u]);
+#if NRNG_POLAR_SPLIT_STOP
+    uint32_t tot = 0;
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) {
+        m[u] = __ballot_sync(kFull, ok[u]);
+        tot += __popc(m[u]);
+    }
+    const bool stop = tot >= cnt - acc;
+#else
+    bool stop;
+    used = polar_rank(ok, m, cnt - acc, lt, stop);
+#endif
+    double ox[kPU], oy[kPU];
+    if constexpr (M == 5)
+        p2_transform_compact<kPU>(c, ok, tp, tab, scr, lane, lt, ox, oy);
+    else
+        polar_transform<kPU>(c, tp, tab, ox, oy);
+#if NRNG_POLAR_SPLIT_STOP
+    if (__builtin_expect(!stop, 1)) {
+        pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, k);
+        used = 32 * kPU;
+    } else {
+        used = polar_trim(ok, m, cnt - acc, lt);
+        pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, k);
+    }
+#else
+    pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, k);
+#endif
     __syncwarp();
     return stop;
 }
