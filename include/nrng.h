@@ -153,6 +153,13 @@ int nrng_set_state(nrng_handle h, const uint64_t* host_ring, const uint64_t* hos
 int nrng_synchronize(nrng_handle h);
 /* Number of kernels this handle has launched since creation (instrumentation). */
 uint64_t nrng_kernel_launches(nrng_handle h);
+/* Race-detector result of a DEBUG build (-DNRNG_RACECHECK=1, csrc/nrng_racecheck.cuh: every
+ * shared-memory window / scratch access of the warp-per-stream kernels is checked against the
+ * __syncwarp() epochs of the other lanes): host_out3[0] = races seen since the last call,
+ * [1] = the first one (source line << 32 | kind << 16 | lane << 8 | other lane; kind 1 RAW,
+ * 2 WAW, 3 WAR), [2] = accesses checked; the counters are then cleared.  Synchronises the
+ * device.  The product build has no detector: zeros and NRNG_EINVAL. */
+int nrng_racecheck_result(uint64_t* host_out3);
 
 /* ---- test hooks (same partition rule; used by the parity tests) ---- */
 /* n uniforms in [0,1), one per slot, stream-major (bit-exact with the oracle). */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "nrng_set_state": ([_p, _p, _p], _int),
     "nrng_synchronize": ([_p], _int),
     "nrng_kernel_launches": ([_p], _u64),
+    "nrng_racecheck_result": ([_p], _int),
     "nrng_uniform": ([_p, _p, _sz], _int),
     "nrng_polar_mask": ([_p, _p, _sz], _int),
     "nrng_transform_from_uniforms": ([_p, _sz, _p, _p, _dbl, _dbl, _int, _p], _int),
@@ -75,6 +76,8 @@ def lib():
                               "(no CPU fallback exists)")
         L = C.CDLL(LIB_PATH)
         for name, (args, res) in SIGNATURES.items():
+            if os.environ.get("NRNG_LIB_OVERRIDE") and not hasattr(L, name):
+                continue  # an older A/B build without a newer entry point
             f = getattr(L, name)
             f.argtypes = args
             f.restype = res
@@ -204,6 +207,14 @@ def nrng_synchronize(h) -> None:
 
 def nrng_kernel_launches(h) -> int:
     return int(lib().nrng_kernel_launches(h))
+
+
+def nrng_racecheck_result():
+    """(races, first race code, accesses checked) of a NRNG_RACECHECK debug build; raises
+    NrngError(EINVAL) on the product build."""
+    out = np.zeros(3, np.uint64)
+    _check(lib().nrng_racecheck_result(out.ctypes.data), "nrng_racecheck_result")
+    return int(out[0]), int(out[1]), int(out[2])
 
 
 def nrng_stream_counts(h) -> np.ndarray:

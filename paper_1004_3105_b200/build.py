@@ -12,7 +12,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc", "nrng.cu")
 DEPS = [SRC, os.path.join(PKG, "csrc", "nrng_kernels.cuh"), os.path.join(PKG, "csrc", "nrng_device.cuh"),
-        os.path.join(PKG, "csrc", "nrng_coeffs.cuh"), os.path.join(ROOT, "include", "nrng.h")]
+        os.path.join(PKG, "csrc", "nrng_coeffs.cuh"), os.path.join(PKG, "csrc", "nrng_racecheck.cuh"),
+        os.path.join(ROOT, "include", "nrng.h")]
 LIB = os.path.join(PKG, "libnrng.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

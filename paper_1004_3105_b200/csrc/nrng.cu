@@ -44,6 +44,32 @@ constexpr size_t kUniSmem = win_bytes(kWarpsPerBlock);
 constexpr size_t kInitSmem = kWarpsPerBlock * kPitch * sizeof(uint64_t);
 constexpr size_t kStageDoubles = size_t(1) << 24;  // 128 MB per staging buffer (host-output path)
 
+#if NRNG_RACECHECK
+// Debug build only (nrng_racecheck.cuh): the shadow arrays, allocated once, cleared before every
+// instrumented launch; races accumulate until read by nrng_racecheck_result.
+RcState g_rc_host{};
+bool rc_ready() {
+    if (g_rc_host.w) return true;
+    const size_t words = (size_t)kRcMaxBlocks * kRcShadowWords;
+    if (cudaMalloc(&g_rc_host.w, words * 8) != cudaSuccess || cudaMalloc(&g_rc_host.r, words * 8) != cudaSuccess ||
+        cudaMalloc(&g_rc_host.epoch, (size_t)kRcMaxThreads * 4) != cudaSuccess ||
+        cudaMalloc(&g_rc_host.races, 16) != cudaSuccess || cudaMalloc(&g_rc_host.checks, 8) != cudaSuccess)
+        return false;
+    cudaMemset(g_rc_host.races, 0, 16);
+    cudaMemset(g_rc_host.checks, 0, 8);
+    return cudaMemcpyToSymbol(g_rc, &g_rc_host, sizeof(g_rc_host)) == cudaSuccess;
+}
+void rc_reset(cudaStream_t st) {
+    if (!rc_ready()) return;
+    const size_t words = (size_t)kRcMaxBlocks * kRcShadowWords;
+    cudaMemsetAsync(g_rc_host.w, 0, words * 8, st);
+    cudaMemsetAsync(g_rc_host.r, 0, words * 8, st);
+    cudaMemsetAsync(g_rc_host.epoch, 0, (size_t)kRcMaxThreads * 4, st);
+}
+#else
+void rc_reset(cudaStream_t) {}
+#endif
+
 struct Occ {
     int bm[4] = {0, 0, 0, 0}, pw[3] = {0, 0, 0}, tri = 0, polar = 0, ratio = 0, ratio1 = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
 };
@@ -185,6 +211,7 @@ void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t 
 }
 
 cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st) {
+    rc_reset(st);
     uint32_t ns = p.s_end - p.s_begin;
     const uint64_t qmax = eff_qmax(p);
     if (kind != Kind::UNIFORM && qmax >= kMidMinPairs && qmax <= kMidMaxPairs && NRNG_MID_MAX > 0) {
@@ -421,6 +448,7 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
         set_err(NRNG_ENOMEM);
         return nullptr;
     }
+    rc_reset(h->stream);
     init_kernel<<<grid_for(S, kWarpsPerBlock, h->occ.init, h->num_sms), kWarpsPerBlock * 32, kInitSmem, h->stream>>>(
         h->ring, h->count, seed, first, S);
     h->launches += 1;
@@ -622,6 +650,7 @@ int nrng_polar_mask(nrng_handle h, uint8_t* dev_mask, size_t cand_per_stream) {
     p.count = h->count;
     p.s_begin = 0;
     p.s_end = h->S;
+    rc_reset(h->stream);
     polar_mask_kernel<<<grid_for(h->S, kWarpsPerBlock, h->occ.mask, h->num_sms), kWarpsPerBlock * 32, kUniSmem,
                         h->stream>>>(
         p, dev_mask, cand_per_stream);
@@ -637,8 +666,8 @@ int nrng_transform_from_uniforms(const double* dev_u, size_t n_pairs, double* de
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) != cudaSuccess) return set_err(NRNG_ENODEV);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned grid = (unsigned)std::min<uint64_t>((n_pairs + 255) / 256, (uint64_t)sms * 8);
-    transform_kernel<<<grid, 256, 0, (cudaStream_t)cuda_stream>>>(dev_u, n_pairs, dev_out, dev_mask,
+    const unsigned grid = (unsigned)std::min<uint64_t>((n_pairs + kTransformThreads - 1) / kTransformThreads, (uint64_t)sms * 8);
+    transform_kernel<<<grid, kTransformThreads, 0, (cudaStream_t)cuda_stream>>>(dev_u, n_pairs, dev_out, dev_mask,
                                                                   TParams{mu, sigma, sigma * 0x1.6a09e667f3bcdp+0}, method);
     return cuda_err(cudaGetLastError());
 }
@@ -659,7 +688,7 @@ int nrng_stats(const double* dev_x, size_t n, double center, const double* dev_e
     if (e == cudaSuccess) {
         stats_partial_kernel<<<nblocks, kStatsThreads, 0, st>>>(dev_x, n, center, dev_edges, K, partial,
                                                                reinterpret_cast<unsigned long long*>(dev_hist));
-        stats_final_kernel<<<1, 32, 0, st>>>(partial, nblocks, dev_sums);
+        stats_final_kernel<<<1, kStatsFinalThreads, 0, st>>>(partial, nblocks, dev_sums);
         e = cudaGetLastError();
     }
     if (partial) cudaFreeAsync(partial, st);
@@ -695,6 +724,22 @@ int nrng_serial_corr(const double* dev_x, size_t n, double center, int K, double
 size_t nrng_serial_corr_blocks(size_t n) {
     const uint64_t tiles = (n + kCorrTile - 1) / kCorrTile;
     return (size_t)std::min<uint64_t>(tiles, kCorrGrid);
+}
+
+int nrng_racecheck_result(uint64_t* host_out3) {
+    if (!host_out3) return set_err(NRNG_EINVAL);
+    host_out3[0] = host_out3[1] = host_out3[2] = 0;
+#if NRNG_RACECHECK
+    if (!rc_ready()) return set_err(NRNG_ENOMEM);
+    cudaDeviceSynchronize();
+    cudaError_t e = cudaMemcpy(host_out3, g_rc_host.races, 16, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(host_out3 + 2, g_rc_host.checks, 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemset(g_rc_host.races, 0, 16);
+    if (e == cudaSuccess) e = cudaMemset(g_rc_host.checks, 0, 8);
+    return cuda_err(e);
+#else
+    return set_err(NRNG_EINVAL);  // not a NRNG_RACECHECK build
+#endif
 }
 
 int nrng_last_error(void) { return g_last; }

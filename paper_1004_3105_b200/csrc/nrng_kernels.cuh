@@ -81,6 +81,15 @@ __device__ __forceinline__ void prefetch_state(const BulkParams& p, uint32_t kn,
     if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.count + kn));
 }
 
+// The first stream of each warp: its state prefetch is issued before the block loads its ln table,
+// so the two global latencies overlap (calls with few streams per warp are latency-bound).
+__device__ __forceinline__ void prefetch_first_state(const BulkParams& p, uint32_t k, int lane) {
+    if (k >= p.s_end) return;
+    const char* row = reinterpret_cast<const char*>(p.ring + (uint64_t)k * kPitch);
+    for (int l = lane; l < 38; l += 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 128 * l));
+    if (lane == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.count + k));
+}
+
 __global__ void __launch_bounds__(kWarpsPerBlock * 32) init_kernel(uint64_t* __restrict__ ring,
                                                                    uint64_t* __restrict__ count, uint64_t seed,
                                                                    uint64_t first_stream, uint32_t S) {
@@ -92,25 +101,25 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) init_kernel(uint64_t* __r
         uint64_t odd = 0;
         for (int j = lane; j < kLagR; j += 32) {
             uint64_t x = splitmix64_mix(seed + ((uint64_t)kLagR * g + j + 1) * kGamma);
-            buf[j] = x;
+            NRNG_ST(&buf[j], x);
             odd |= x & 1;
         }
         const bool any_odd = __any_sync(kFull, odd != 0);
-        __syncwarp();
-        if (!any_odd && lane == 0) buf[0] |= 1;
-        __syncwarp();
+        NRNG_SYNCWARP();
+        if (!any_odd && lane == 0) NRNG_ST(&buf[0], NRNG_LD(&buf[0]) | 1);
+        NRNG_SYNCWARP();
         for (int r = 0; r < 10; ++r) {
-            for (int i = lane; i < kLagS; i += 32) buf[i] += buf[i + (kLagR - kLagS)];
-            __syncwarp();
-            for (int i = kLagS + lane; i < 2 * kLagS; i += 32) buf[i] += buf[i - kLagS];
-            __syncwarp();
-            for (int i = 2 * kLagS + lane; i < kLagR; i += 32) buf[i] += buf[i - kLagS];
-            __syncwarp();
+            for (int i = lane; i < kLagS; i += 32) NRNG_ST(&buf[i], NRNG_LD(&buf[i]) + NRNG_LD(&buf[i + (kLagR - kLagS)]));
+            NRNG_SYNCWARP();
+            for (int i = kLagS + lane; i < 2 * kLagS; i += 32) NRNG_ST(&buf[i], NRNG_LD(&buf[i]) + NRNG_LD(&buf[i - kLagS]));
+            NRNG_SYNCWARP();
+            for (int i = 2 * kLagS + lane; i < kLagR; i += 32) NRNG_ST(&buf[i], NRNG_LD(&buf[i]) + NRNG_LD(&buf[i - kLagS]));
+            NRNG_SYNCWARP();
         }
         uint64_t* rk = ring + (uint64_t)k * kPitch;
-        for (int j = lane; j < kPitch; j += 32) rk[j] = j < kLagR ? buf[j] : 0;
+        for (int j = lane; j < kPitch; j += 32) rk[j] = j < kLagR ? NRNG_LD(&buf[j]) : 0;
         if (lane == 0) count[k] = 0;
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 }
 
@@ -130,16 +139,16 @@ __device__ __forceinline__ void bm_pairs(const uint64_t* src, const TParams& tp,
         uint64_t w1[U], w2[U], w3[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            w1[u] = src[32 * per * u];
-            w2[u] = src[32 * per * u + 1];
-            w3[u] = src[32 * per * u + 2];
+            w1[u] = NRNG_LD(&src[32 * per * u]);
+            w2[u] = NRNG_LD(&src[32 * per * u + 1]);
+            w3[u] = NRNG_LD(&src[32 * per * u + 2]);
         }
         b3_pairs<U>(w1, w2, w3, tp, tab, x, y);
     } else {
         uint64_t wu[U], wv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const ulonglong2 xw = *reinterpret_cast<const ulonglong2*>(src + 32 * per * u);
+            const ulonglong2 xw = NRNG_LD(reinterpret_cast<const ulonglong2*>(src + 32 * per * u));
             wu[u] = xw.x;
             wv[u] = xw.y;
         }
@@ -163,7 +172,8 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
     constexpr uint32_t kNeedU = 32 * kU * per;         // words per main-loop iteration
     static_assert(kNeedU - 1 + kB <= kWin - kLagR, "lookahead would clobber the write-back words");
     static_assert(kNeedU <= kMirror, "unmasked reads must stay inside the mirror");
-    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
+    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + (threadIdx.x >> 5), threadIdx.x & 31);
+    const Tables tab = load_tables<NW * 32>(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
     __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
                     phase_gen_store(bl, nb, g);
 #pragma unroll
                     for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
-                    __syncwarp();
+                    NRNG_SYNCWARP();
                     ph = nb;
                 }
                 L.wc = kW0 + (uint32_t)(per * full);
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
                     for (int u = 0; u < kU; ++u)
                         if (x[u] == 1234.5 && y[u] == 1234.5) __stcs(o + 32 * u, make_double2(x[u], y[u]));
 #endif
-                    __syncwarp();
+                    NRNG_SYNCWARP();
                     ph = (ph + 1) & 3;
                 }
                 L.wc = L.wg = kW0 + (uint32_t)(per * full);
@@ -257,7 +267,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
 #pragma unroll
                 for (int u = 0; u < kU; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
                 L.wc += kNeedU;
-                __syncwarp();
+                NRNG_SYNCWARP();
             }
         }
         for (; j0 < qk.cnt; j0 += 32) {
@@ -270,11 +280,11 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlock ? 1 : 5) bm_kernel(Bu
                 store_pair(p.out, 2 * pair_slot(p, qk.off, k, j0 + lane), p.shift, p.n, x[0], y[0], p.aligned);
             }
             L.wc += per * active;
-            __syncwarp();
+            NRNG_SYNCWARP();
         }
         lfg_store(L, rk, C, lane);
         if (lane == 0) p.count[k] = C + (L.wc - kW0);
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 }
 
@@ -336,8 +346,8 @@ __device__ __forceinline__ void gen_tri_rows(uint64_t* buf, const TriPos& ps, in
     for (int t = 0; t < R; ++t) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            a[t][i] = sa[kTriRow * t + i];
-            b[t][i] = sb[kTriRow * t + i];
+            a[t][i] = NRNG_LD(&sa[kTriRow * t + i]);
+            b[t][i] = NRNG_LD(&sb[kTriRow * t + i]);
         }
     }
 #pragma unroll
@@ -347,13 +357,13 @@ __device__ __forceinline__ void gen_tri_rows(uint64_t* buf, const TriPos& ps, in
         w3[t] = a[t][2] + b[t][2];
         const uint32_t pd = t == 0 ? ps.d : tri_wrap(ps.d + kTriRow * t);
         uint64_t* d = buf + pd + 3 * lane;
-        d[0] = w1[t];
-        d[1] = w2[t];
-        d[2] = w3[t];
+        NRNG_ST(&d[0], w1[t]);
+        NRNG_ST(&d[1], w2[t]);
+        NRNG_ST(&d[2], w3[t]);
         if (pd < (uint32_t)kTriMirror) {  // rows 0-1 are mirrored past the end
-            d[kTriWin] = w1[t];
-            d[kTriWin + 1] = w2[t];
-            d[kTriWin + 2] = w3[t];
+            NRNG_ST(&d[kTriWin], w1[t]);
+            NRNG_ST(&d[kTriWin + 1], w2[t]);
+            NRNG_ST(&d[kTriWin + 2], w3[t]);
         }
     }
 }
@@ -370,8 +380,8 @@ __device__ __forceinline__ void gen_tri_half(uint64_t* lb, uint64_t (&w1)[4], ui
     for (int t = 0; t < 2; ++t) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            sa[t][i] = lb[a + kTriRow * t + i];
-            sb[t][i] = lb[b + kTriRow * t + i];
+            sa[t][i] = NRNG_LD(&lb[a + kTriRow * t + i]);
+            sb[t][i] = NRNG_LD(&lb[b + kTriRow * t + i]);
         }
     }
 #pragma unroll
@@ -380,13 +390,13 @@ __device__ __forceinline__ void gen_tri_half(uint64_t* lb, uint64_t (&w1)[4], ui
         w1[r] = sa[t][0] + sb[t][0];
         w2[r] = sa[t][1] + sb[t][1];
         w3[r] = sa[t][2] + sb[t][2];
-        lb[d + kTriRow * t] = w1[r];
-        lb[d + kTriRow * t + 1] = w2[r];
-        lb[d + kTriRow * t + 2] = w3[r];
+        NRNG_ST(&lb[d + kTriRow * t], w1[r]);
+        NRNG_ST(&lb[d + kTriRow * t + 1], w2[r]);
+        NRNG_ST(&lb[d + kTriRow * t + 2], w3[r]);
         if constexpr (d < kTriMirror) {
-            lb[d + kTriWin + kTriRow * t] = w1[r];
-            lb[d + kTriWin + kTriRow * t + 1] = w2[r];
-            lb[d + kTriWin + kTriRow * t + 2] = w3[r];
+            NRNG_ST(&lb[d + kTriWin + kTriRow * t], w1[r]);
+            NRNG_ST(&lb[d + kTriWin + kTriRow * t + 1], w2[r]);
+            NRNG_ST(&lb[d + kTriWin + kTriRow * t + 2], w3[r]);
         }
     }
 }
@@ -397,14 +407,14 @@ __device__ __forceinline__ void b3_iter(uint64_t* lb, const TParams& tp, const T
                                         unsigned lt, double2* o) {
     uint64_t w1[4], w2[4], w3[4];
     gen_tri_half<PH, 0>(lb, w1, w2, w3);
-    __syncwarp();  // rows 2-3 read rows 0-1 (lag 273)
+    NRNG_SYNCWARP();  // rows 2-3 read rows 0-1 (lag 273)
     gen_tri_half<PH, 1>(lb, w1, w2, w3);
     double x[4], y[4];
     b3_pairs_compact<4>(w1, w2, w3, tp, tab, scr, lane, lt, x, y);
 #pragma unroll
     for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
 #if !NRNG_SCR_SYNC_MIN
-    __syncwarp();  // (with NRNG_SCR_SYNC_MIN the gather's __syncwarp, after every window access of
+    NRNG_SYNCWARP();  // (with NRNG_SCR_SYNC_MIN the gather's __syncwarp, after every window access of
 #endif             // this iteration, orders them before the next iteration's window writes)
 }
 
@@ -413,7 +423,8 @@ template <int NW, bool EP = false>  // EP: the sequential mode's epoch layout (s
 __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * (kTriAlloc + kTriScratch)));
+    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + (threadIdx.x >> 5), threadIdx.x & 31);
+    const Tables tab = load_tables<NW * 32>(reinterpret_cast<double2*>(smem + NW * (kTriAlloc + kTriScratch)));
     __syncthreads();
     uint64_t* const buf = smem + warp * (kTriAlloc + kTriScratch);
     double* const scr = reinterpret_cast<double*>(buf + kTriAlloc);
@@ -424,15 +435,9 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
-        {   // x_{C-607+j} -> position 1152 - 607 + j
-            const uint32_t base = (uint32_t)(C % kLagR);
-            for (int j = lane; j < kLagR; j += 32) {
-                uint32_t q = base + j;
-                q = q >= (uint32_t)kLagR ? q - kLagR : q;
-                buf[(kTriWin - kLagR) + j] = rk[q];
-            }
-        }
-        __syncwarp();
+        // x_{C-607+j} -> position 1152 - 607 + j
+        load_state(rk, C, lane, [&](uint32_t j) { return buf + (kTriWin - kLagR) + j; }, all_state_words);
+        NRNG_SYNCWARP();
         prefetch_state<2>(p, k + gridDim.x * NW, lane);
         // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
         const uint64_t safe_cnt = 2 * (qk.off + qk.cnt) <= p.n ? qk.cnt : qk.cnt - 1;
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
             if ((uint64_t)lane < qk2.cnt - j0)
                 store_pair(p.out, 2 * (EP ? pair_slot(p, qk2.off, k, j0 + lane) : qk2.off + j0 + lane), p.shift, p.n,
                            x[0], y[0], true);
-            __syncwarp();
+            NRNG_SYNCWARP();
             ps.advance(1);
         }
         // write back the last min(3 cnt, 607) consumed words (relative index i at i mod 1152)
@@ -486,11 +491,11 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
             uint32_t pp = pos0 + j, q = slot0 + j;
             pp = pp >= (uint32_t)kTriWin ? pp - kTriWin : pp;
             q = q >= (uint32_t)kLagR ? q - kLagR : q;
-            rk2[q] = buf[pp];
+            rk2[q] = NRNG_LD(&buf[pp]);
         }
-        __syncwarp();  // every lane has read count[k] before lane 0 updates it
+        NRNG_SYNCWARP();  // every lane has read count[k] before lane 0 updates it
         if (lane == 0) p.count[k] = C2 + used;
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 }
 
@@ -555,7 +560,8 @@ template <int NW, int M, bool EP = false>  // EP: the sequential mode's whole-ep
 __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
+    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + (threadIdx.x >> 5), threadIdx.x & 31);
+    const Tables tab = load_tables<NW * 32>(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
     __syncthreads();
     WarpLFG L;
     L.buf = smem + warp * kWinAlloc;
@@ -592,7 +598,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
 #ifndef NRNG_EXP_P_NOCONSUME
 #pragma unroll
                 for (int u = 0; u < kPU; ++u) {
-                    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(L.buf + kBlk * ph + 64 * u + 2 * lane);
+                    const ulonglong2 w = NRNG_LD(reinterpret_cast<const ulonglong2*>(L.buf + kBlk * ph + 64 * u + 2 * lane));
                     ok[u] = polar_candidate(w.x, w.y, c[u]);
                 }
 #else  // experiment: candidates from the freshly generated words (no window re-read; wrong stream order)
@@ -624,7 +630,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                         acc += __popc(m[u]);
                     }
                 }
-                __syncwarp();
+                NRNG_SYNCWARP();
                 if (stop) {
                     L.wc = kW0 + kBlk * it + 2 * used;
                     L.wg = kW0 + kBlk * (it + 1);
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 unsigned m[kPU];
 #pragma unroll
                 for (int u = 0; u < kPU; ++u) {
-                    const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(L.at(64 * u + 2 * lane));
+                    const ulonglong2 w = NRNG_LD(reinterpret_cast<const ulonglong2*>(L.at(64 * u + 2 * lane)));
                     ok[u] = polar_candidate(w.x, w.y, c[u]);
                 }
                 bool stop;
@@ -679,13 +685,13 @@ __global__ void __launch_bounds__(NW * 32, NW == kBigBlockPolar ? 1 : 4) polar_k
                 }
                 acc = j;
                 L.wc += 2 * used;
-                __syncwarp();
+                NRNG_SYNCWARP();
             }
             base += cnt;
         }
         lfg_store(L, rk, C, lane);
         if (lane == 0) p.count[k] = C + (L.wc - kW0);
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 }
 
@@ -748,10 +754,10 @@ __device__ __forceinline__ void pw_gen(uint64_t* buf, uint32_t K, const PwLane& 
 #pragma unroll
         for (int t = 0; t < R; ++t) {
             const uint32_t pa = K + 64 * t + (kWin - kLagR) + l2, pb = K + 64 * t + (kWin - kLagS) + l2;
-            a0[t] = buf[swz(pa & kWinMask)];
-            a1[t] = buf[swz((pa + 1) & kWinMask)];
-            b0[t] = buf[swz(pb & kWinMask)];
-            b1[t] = buf[swz((pb + 1) & kWinMask)];
+            a0[t] = NRNG_LD(&buf[swz(pa & kWinMask)]);
+            a1[t] = NRNG_LD(&buf[swz((pa + 1) & kWinMask)]);
+            b0[t] = NRNG_LD(&buf[swz(pb & kWinMask)]);
+            b1[t] = NRNG_LD(&buf[swz((pb + 1) & kWinMask)]);
         }
     } else {
         const int ka = (int)((K + (kWin - kLagR)) & kWinMask) - (kWin - kLagR);  // multiple of 64
@@ -762,10 +768,10 @@ __device__ __forceinline__ void pw_gen(uint64_t* buf, uint32_t K, const PwLane& 
         const uint64_t* pb1 = buf + (kb + (int)o.b1);
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            a0[t] = pa0[64 * t];
-            a1[t] = pa1[64 * t];
-            b0[t] = pb0[64 * t];
-            b1[t] = pb1[64 * t];
+            a0[t] = NRNG_LD(&pa0[64 * t]);
+            a1[t] = NRNG_LD(&pa1[64 * t]);
+            b0[t] = NRNG_LD(&pb0[64 * t]);
+            b1[t] = NRNG_LD(&pb1[64 * t]);
         }
     }
     uint64_t* pd0 = buf + (K + o.d0);
@@ -774,14 +780,14 @@ __device__ __forceinline__ void pw_gen(uint64_t* buf, uint32_t K, const PwLane& 
     for (int t = 0; t < R; ++t) {
         w0[t] = a0[t] + b0[t];
         w1[t] = a1[t] + b1[t];
-        pd0[64 * t] = w0[t];
-        pd1[64 * t] = w1[t];
+        NRNG_ST(&pd0[64 * t], w0[t]);
+        NRNG_ST(&pd1[64 * t], w1[t]);
     }
     if (!kNoMirror && K < (uint32_t)kMirror) {  // rows in [0, 256): mirrored at +1024
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            pd0[kWin + 64 * t] = w0[t];
-            pd1[kWin + 64 * t] = w1[t];
+            NRNG_ST(&pd0[kWin + 64 * t], w0[t]);
+            NRNG_ST(&pd1[kWin + 64 * t], w1[t]);
         }
     }
 }
@@ -816,10 +822,10 @@ __device__ __forceinline__ void pw_load_row(const PwPtrs& pp, uint64_t& a0, uint
     constexpr int oa = ka + 64 * T - (sa >= kWin ? kWin : 0);
     constexpr int ob = kb + 64 * T - (sb >= kWin ? kWin : 0);
     constexpr bool xa = sa < kWin && sa + 64 > kWin, xb = sb < kWin && sb + 64 > kWin;
-    a0 = (xa ? pp.a0x : pp.a0)[oa];
-    a1 = (xa ? pp.a1x : pp.a1)[oa];
-    b0 = (xb ? pp.b0x : pp.b0)[ob];
-    b1 = (xb ? pp.b1x : pp.b1)[ob];
+    a0 = NRNG_LD(&(xa ? pp.a0x : pp.a0)[oa]);
+    a1 = NRNG_LD(&(xa ? pp.a1x : pp.a1)[oa]);
+    b0 = NRNG_LD(&(xb ? pp.b0x : pp.b0)[ob]);
+    b1 = NRNG_LD(&(xb ? pp.b1x : pp.b1)[ob]);
 }
 template <int K, int R, int... T>
 __device__ __forceinline__ void pw_load_rows(const PwPtrs& pp, uint64_t (&a0)[R], uint64_t (&a1)[R], uint64_t (&b0)[R],
@@ -838,21 +844,21 @@ __device__ __forceinline__ void pw_gen_c(const PwPtrs& pp, uint64_t (&w0)[R], ui
     } else {
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            a0[t] = pp.a0[ka + 64 * t];
-            a1[t] = pp.a1[ka + 64 * t];
-            b0[t] = pp.b0[kb + 64 * t];
-            b1[t] = pp.b1[kb + 64 * t];
+            a0[t] = NRNG_LD(&pp.a0[ka + 64 * t]);
+            a1[t] = NRNG_LD(&pp.a1[ka + 64 * t]);
+            b0[t] = NRNG_LD(&pp.b0[kb + 64 * t]);
+            b1[t] = NRNG_LD(&pp.b1[kb + 64 * t]);
         }
     }
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         w0[t] = a0[t] + b0[t];
         w1[t] = a1[t] + b1[t];
-        pp.d0[K + 64 * t] = w0[t];
-        pp.d1[K + 64 * t] = w1[t];
+        NRNG_ST(&pp.d0[K + 64 * t], w0[t]);
+        NRNG_ST(&pp.d1[K + 64 * t], w1[t]);
         if (!NRNG_PW_NOMIRROR && K < kMirror) {
-            pp.d0[K + kWin + 64 * t] = w0[t];
-            pp.d1[K + kWin + 64 * t] = w1[t];
+            NRNG_ST(&pp.d0[K + kWin + 64 * t], w0[t]);
+            NRNG_ST(&pp.d1[K + kWin + 64 * t], w1[t]);
         }
     }
 }
@@ -872,34 +878,34 @@ __device__ __forceinline__ void pw_gen_r(const PwPtrs& pp, uint32_t ph, uint64_t
     uint64_t a0[R], a1[R], b0[R], b1[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) {
-        a0[t] = pp.a0[kk.x + 64 * t];
-        a1[t] = pp.a1[kk.x + 64 * t];
-        b0[t] = pp.b0[kk.y + 64 * t];
-        b1[t] = pp.b1[kk.y + 64 * t];
+        a0[t] = NRNG_LD(&pp.a0[kk.x + 64 * t]);
+        a1[t] = NRNG_LD(&pp.a1[kk.x + 64 * t]);
+        b0[t] = NRNG_LD(&pp.b0[kk.y + 64 * t]);
+        b1[t] = NRNG_LD(&pp.b1[kk.y + 64 * t]);
     }
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         w0[t] = a0[t] + b0[t];
         w1[t] = a1[t] + b1[t];
-        pp.d0[K + 64 * t] = w0[t];
-        pp.d1[K + 64 * t] = w1[t];
+        NRNG_ST(&pp.d0[K + 64 * t], w0[t]);
+        NRNG_ST(&pp.d1[K + 64 * t], w1[t]);
     }
 #if NRNG_B1_MIRROR_BRANCH  // a real branch: the mirror stores are skipped in 3 blocks of 4
     if (__builtin_expect(ph == 0, 0)) {
         asm volatile("" ::: "memory");
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            pp.d0[kWin + 64 * t] = w0[t];
-            pp.d1[kWin + 64 * t] = w1[t];
+            NRNG_ST(&pp.d0[kWin + 64 * t], w0[t]);
+            NRNG_ST(&pp.d1[kWin + 64 * t], w1[t]);
         }
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 #else
     if (ph == 0) {
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            pp.d0[kWin + 64 * t] = w0[t];
-            pp.d1[kWin + 64 * t] = w1[t];
+            NRNG_ST(&pp.d0[kWin + 64 * t], w0[t]);
+            NRNG_ST(&pp.d1[kWin + 64 * t], w1[t]);
         }
     }
 #endif
@@ -917,7 +923,7 @@ __device__ __forceinline__ void pw_bm_block(const PwPtrs& pp, const TParams& tp,
         b2_pairs<4>(wu, wv, tp, tab, x, y);
 #pragma unroll
     for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
-    __syncwarp();
+    NRNG_SYNCWARP();
 }
 
 // The accepts of one step trimmed to the remaining quota `need` (exact stop, R5): m[u] keeps
@@ -1022,7 +1028,7 @@ __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& 
 #else
     pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, k);
 #endif
-    __syncwarp();
+    NRNG_SYNCWARP();
     return stop;
 }
 
@@ -1045,7 +1051,7 @@ __device__ __forceinline__ bool pw_ratio_block(const PwPtrs& pp, const TParams& 
         if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), __fma_rn(tp.sigma, x[u], tp.mu));
         acc += __popc(m[u]);
     }
-    __syncwarp();
+    NRNG_SYNCWARP();
     return stop;
 }
 
@@ -1070,7 +1076,7 @@ __device__ __forceinline__ bool pw_ratio1_block(const PwPtrs& pp, const TParams&
         if ((m[u] >> lane) & 1u) __stcs(o + (acc + __popc(m[u] & lt)), __fma_rn(tp.sigma, x[u], tp.mu));
         acc += __popc(m[u]);
     }
-    __syncwarp();
+    NRNG_SYNCWARP();
     return stop;
 }
 
@@ -1081,7 +1087,8 @@ template <int M, int NW, bool EP = false>
 __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const Tables tab = load_tables(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
+    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + (threadIdx.x >> 5), threadIdx.x & 31);
+    const Tables tab = load_tables<NW * 32>(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
     __syncthreads();
     uint64_t* const buf = smem + warp * kWinAlloc;
     const PwLane ol = pw_lane(lane);
@@ -1094,15 +1101,9 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
         if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<1>(p, k + gridDim.x * NW, lane);
         const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
-        {   // x_{C-607+j} -> logical position 417 + j
-            const uint32_t base = (uint32_t)(C % kLagR);
-            for (int j = lane; j < kLagR; j += 32) {
-                uint32_t q = base + j;
-                q = q >= (uint32_t)kLagR ? q - kLagR : q;
-                buf[swz((kWin - kLagR) + j)] = rk[q];
-            }
-        }
-        __syncwarp();
+        // x_{C-607+j} -> logical position 417 + j
+        load_state(rk, C, lane, [&](uint32_t j) { return buf + swz((kWin - kLagR) + j); }, all_state_words);
+        NRNG_SYNCWARP();
         if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<2>(p, k + gridDim.x * NW, lane);
         uint64_t used;  // words consumed by this call
         if constexpr (M <= 2) {
@@ -1146,7 +1147,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
                     b2_pairs<4>(wu, wv, p.tp, tab, x, y);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) __stcs(o + 32 * u, make_double2(x[u], y[u]));
-                __syncwarp();
+                NRNG_SYNCWARP();
             }
             uint32_t K = (256 * b) & kWinMask;
             for (uint64_t j0 = 128ull * b; j0 < qk.cnt; j0 += 32) {  // last rows, partial, unsafe pair
@@ -1160,7 +1161,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
                 if ((uint64_t)lane < qk.cnt - j0)
                     store_pair(p.out, 2 * (EP ? pair_slot(p, qk.off, k, j0 + lane) : qk.off + j0 + lane), p.shift, p.n,
                                x[0], y[0], true);
-                __syncwarp();
+                NRNG_SYNCWARP();
                 K = (K + 64) & kWinMask;
             }
             used = 2 * qk.cnt;
@@ -1221,10 +1222,10 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
         for (uint32_t j = lane; j < nw; j += 32) {
             uint32_t q = slot0 + j;
             q = q >= (uint32_t)kLagR ? q - kLagR : q;
-            rk[q] = buf[swz((pos0 + j) & kWinMask)];
+            rk[q] = NRNG_LD(&buf[swz((pos0 + j) & kWinMask)]);
         }
         if (lane == 0) p.count[k] = C + used;
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 }
 
@@ -1277,7 +1278,7 @@ __device__ __forceinline__ void ring_commit(uint64_t* __restrict__ r, uint32_t& 
 template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2; 6 = R (units: normals, one per accept)
 __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
     __shared__ double2 tabs[kTabBytes / 16];
-    const Tables tab = load_tables(tabs);
+    const Tables tab = load_tables<kTinyThreads>(tabs);
     __syncthreads();
     const uint32_t k = p.s_begin + blockIdx.x * kTinyThreads + threadIdx.x;
     if (k >= p.s_end) return;
@@ -1393,7 +1394,7 @@ constexpr uint64_t kMidMinPairs = NRNG_MID_MIN, kMidMaxPairs = NRNG_MID_MAX;  //
 template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2; 6 = R (units: normals, one per accept)
 __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
     __shared__ double2 tabs[kTabBytes / 16];
-    const Tables tab = load_tables(tabs);
+    const Tables tab = load_tables<kMidWarps * 32>(tabs);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt(lane);
@@ -1486,10 +1487,10 @@ __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
                 for (int t = 0; t < per; ++t) r[pa[t]] = w[t];
             }
             i0 += words;
-            __syncwarp();
+            NRNG_SYNCWARP();
         }
         if (lane == 0) p.count[k] = C + i0;
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 }
 
@@ -1513,14 +1514,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) uniform_kernel(BulkParams
             const uint32_t active = left < 32 ? (uint32_t)left : 32u;
             if ((uint32_t)lane < active) {
                 const uint64_t g = qk.off + j0 + lane;
-                p.out[g - p.shift] = (double)ukey(L.buf[(L.wc + lane) & kWinMask]) * 0x1p-53;  // exact
+                p.out[g - p.shift] = (double)ukey(NRNG_LD(&L.buf[(L.wc + lane) & kWinMask])) * 0x1p-53;  // exact
             }
             L.wc += active;
-            __syncwarp();
+            NRNG_SYNCWARP();
         }
         lfg_store(L, rk, C, lane);
         if (lane == 0) p.count[k] = C + (L.wc - kW0);
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 }
 
@@ -1541,27 +1542,28 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32) polar_mask_kernel(BulkPar
             const uint64_t left = cand - j0;
             const uint32_t active = left < 32 ? (uint32_t)left : 32u;
             if ((uint32_t)lane < active) {
-                const ulonglong2 xw = *reinterpret_cast<const ulonglong2*>(&L.buf[(L.wc + 2 * lane) & kWinMask]);
+                const ulonglong2 xw = NRNG_LD(reinterpret_cast<const ulonglong2*>(&L.buf[(L.wc + 2 * lane) & kWinMask]));
                 PolarCand pc;
                 mask[(uint64_t)k * cand + j0 + lane] = polar_candidate(xw.x, xw.y, pc) ? 1 : 0;
             }
             L.wc += 2 * active;
-            __syncwarp();
+            NRNG_SYNCWARP();
         }
         lfg_store(L, rk, C, lane);
         if (lane == 0) p.count[k] = C + (L.wc - kW0);
-        __syncwarp();
+        NRNG_SYNCWARP();
     }
 }
 
 // nrng_transform_from_uniforms: one thread per pair; the given uniforms (multiples of
 // 2^-53 in [0,1)) are turned back into the words the stream would hold, so this runs
 // exactly the device code of the bulk kernels.
+constexpr int kTransformThreads = 256;
 __device__ __forceinline__ uint64_t word_of(double u) { return __double2ull_rn(u * 0x1p53) << 11; }
-__global__ void transform_kernel(const double* __restrict__ u, uint64_t n_pairs, double* __restrict__ out,
+__global__ void __launch_bounds__(kTransformThreads) transform_kernel(const double* __restrict__ u, uint64_t n_pairs, double* __restrict__ out,
                                  uint8_t* __restrict__ mask, TParams tp, int method) {
     __shared__ double2 tabs[kTabBytes / 16];
-    const Tables tab = load_tables(tabs);
+    const Tables tab = load_tables<kTransformThreads>(tabs);
     __syncthreads();
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_pairs;
          j += (uint64_t)gridDim.x * blockDim.x) {
@@ -1724,20 +1726,34 @@ __global__ void __launch_bounds__(kStatsThreads) stats_partial_kernel(const doub
 }
 
 // sums[0..3] = the compensated power sums (sum + accumulated error), sums[4] = min, [5] = max.
-__global__ void stats_final_kernel(const double* __restrict__ partial, int nblocks, double* __restrict__ sums) {
-    const int t = threadIdx.x;
+// Warp t reduces quantity t: lane l combines blocks l, l + 32, ... in order, then a fixed
+// xor-shuffle tree combines the lanes (a deterministic order for a given block count).
+constexpr int kStatsFinalThreads = 6 * 32;
+__global__ void __launch_bounds__(kStatsFinalThreads) stats_final_kernel(const double* __restrict__ partial,
+                                                                         int nblocks, double* __restrict__ sums) {
+    const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (t < 4) {
-        double v = partial[t], c = partial[4 + t];
-        for (int b = 1; b < nblocks; ++b) {
+        double v = 0.0, c = 0.0;
+        for (int b = lane; b < nblocks; b += 32) {
             comp_add(v, c, partial[b * kStatsPartial + t]);
             c = __dadd_rn(c, partial[b * kStatsPartial + 4 + t]);
         }
-        sums[t] = __dadd_rn(v, c);
-    } else if (t < 6) {
-        double v = partial[4 + t];
-        for (int b = 1; b < nblocks; ++b) v = t == 4 ? fmin(v, partial[b * kStatsPartial + 4 + t])
-                                                     : fmax(v, partial[b * kStatsPartial + 4 + t]);
-        sums[t] = v;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ws = __shfl_xor_sync(kFull, v, o), wc = __shfl_xor_sync(kFull, c, o);
+            comp_add(v, c, ws);
+            c = __dadd_rn(c, wc);
+        }
+        if (lane == 0) sums[t] = __dadd_rn(v, c);
+    } else {
+        const int q = 4 + t;  // 8: min, 9: max
+        double v = t == 4 ? __longlong_as_double(0x7ff0000000000000ULL) : __longlong_as_double(0xfff0000000000000ULL);
+        for (int b = lane; b < nblocks; b += 32)
+            v = t == 4 ? fmin(v, partial[b * kStatsPartial + q]) : fmax(v, partial[b * kStatsPartial + q]);
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_xor_sync(kFull, v, o);
+            v = t == 4 ? fmin(v, w) : fmax(v, w);
+        }
+        if (lane == 0) sums[t] = v;
     }
 }
 

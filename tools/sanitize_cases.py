@@ -50,7 +50,7 @@ def main():
         run(g, m, per * 64 * 3 + 1)                     # tiny_kernel
     for m in ("B1", "B2", "B3", "P", "P2"):             # sequential mode, whole epochs (EP kernels)
         g = P.Generator(3, 3000)
-        x = g.normal_seq(m, 2 * 3000 * 128 + 5)
+        x = g.normal_seq(m, 3 * 2 * 3000 * 128 + 5)  # 3 whole epochs in one launch: the EP kernels
         torch.cuda.synchronize()
         assert torch.isfinite(x).all()
     g = P.Generator(4, 600)
