@@ -189,8 +189,9 @@ def time_configs(P, torch, big, hbm_gbs, fp64_peak, sweep_calls=1000):
     stream = torch.cuda.current_stream()
 
     def timed(g, m, n, mu, sigma, calls, graph=False):
+        o = big[:n]  # the caller's buffer, allocated once
         for _ in range(3):
-            g.normal(m, out=big[:n], mu=mu, sigma=sigma)
+            g.normal(m, out=o, mu=mu, sigma=sigma)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if graph:
             gr, s2 = torch.cuda.CUDAGraph(), torch.cuda.Stream()
@@ -198,7 +199,7 @@ def time_configs(P, torch, big, hbm_gbs, fp64_peak, sweep_calls=1000):
             with torch.cuda.stream(s2):
                 with torch.cuda.graph(gr, stream=s2):
                     for _ in range(calls):
-                        g.normal(m, out=big[:n], mu=mu, sigma=sigma)
+                        g.normal(m, out=o, mu=mu, sigma=sigma)
             stream.wait_stream(s2)
             torch.cuda.synchronize()
             a.record(stream)
@@ -208,7 +209,7 @@ def time_configs(P, torch, big, hbm_gbs, fp64_peak, sweep_calls=1000):
             torch.cuda.synchronize()
             a.record(stream)
             for _ in range(calls):
-                g.normal(m, out=big[:n], mu=mu, sigma=sigma)
+                g.normal(m, out=o, mu=mu, sigma=sigma)
             b.record(stream)
         torch.cuda.synchronize()
         t = a.elapsed_time(b) / calls / 1e3
@@ -229,6 +230,8 @@ def time_configs(P, torch, big, hbm_gbs, fp64_peak, sweep_calls=1000):
         g = P.Generator(c.seed, c.streams)
         for m in c.methods:
             res["%s_%s" % (c.name, m)] = timed(g, m, c.n, c.mu, c.sigma, 20)
+            if c.n <= (1 << 24):  # launch-latency-sized calls: also inside one CUDA graph
+                res["%s_%s_graph" % (c.name, m)] = timed(g, m, c.n, c.mu, c.sigma, 20, graph=True)
         g.close()
     c = W.C4
     g = P.Generator(c.seed, c.streams)

@@ -291,10 +291,22 @@ class Generator:
         if not torch.cuda.is_available():
             raise RuntimeError("paper_1004_3105_b200 needs a CUDA device (no CPU fallback)")
         self.seed, self.S, self.first, self.variant = int(seed), int(n_streams), int(first_stream), int(variant)
-        self.device = torch.device("cuda", torch.cuda.current_device())
+        self._dev = torch.cuda.current_device()
+        self.device = torch.device("cuda", self._dev)
         self.h = nrng_create_range(self.seed, self.first, self.S, self.variant)
-        self._stream = _stream_ptr(torch)
+        self._torch = torch
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        self._raw_stream = (lambda: raw(self._dev)) if raw is not None else (
+            lambda: torch.cuda.current_stream(self._dev).cuda_stream)
+        self._stream = self._raw_stream()
         nrng_set_stream(self.h, self._stream)
+        L = lib()
+        # per method: (C entry point, trailing arguments, name for errors); the short-call path
+        # below costs a few microseconds of host time per call, so it avoids per-call lookups
+        bm = L.nrng_normal_boxmuller
+        self._calls = {"B1": (bm, (1,)), "B2": (bm, (2,)), "B3": (bm, (3,)),
+                       "P": (L.nrng_normal_polar, ()), "P2": (L.nrng_normal_polar2, ()),
+                       "R": (L.nrng_normal_ratio, ()), "R1": (L.nrng_normal_ratio1, ())}
 
     def close(self):
         if getattr(self, "h", None):
@@ -308,16 +320,31 @@ class Generator:
             pass
 
     def _sync_stream(self):
-        sp = _stream_ptr(_torch())
+        sp = self._raw_stream()
         if sp != self._stream:  # the handle keeps its stream: only tell it about changes
             nrng_set_stream(self.h, sp)
             self._stream = sp
 
     def _out(self, n, out):
+        torch = self._torch
         if out is None:
-            out = _torch().empty(n, dtype=_torch().float64, device=self.device)
+            out = torch.empty(n, dtype=torch.float64, device=self.device)
+            return out, out.data_ptr(), n
+        if type(out) is torch.Tensor and out.is_cuda:  # fast path of out_buffer's checks
+            if out.dtype is not torch.float64 or not out.is_contiguous() or out.get_device() != self._dev:
+                out_buffer(out, self.device)  # raises with the reason
+            return out, out.data_ptr(), out.numel()
         ptr, size = out_buffer(out, self.device)
         return out, ptr, size
+
+    def _call(self, key, n, mu, sigma, out):
+        fn, extra = self._calls[key]
+        out, ptr, n = self._out(n, out)
+        self._sync_stream()
+        rc = fn(self.h, ptr, n, mu, sigma, *extra)
+        if rc:
+            raise NrngError(rc, fn.__name__)
+        return out
 
     def normal_boxmuller(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, variant: int = 0, out=None):
         out, ptr, n = self._out(n, out)
@@ -326,41 +353,23 @@ class Generator:
         return out
 
     def normal_polar(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
-        out, ptr, n = self._out(n, out)
-        self._sync_stream()
-        nrng_normal_polar(self.h, ptr, n, mu, sigma)
-        return out
+        return self._call("P", n, mu, sigma, out)
 
     def normal_polar2(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
-        out, ptr, n = self._out(n, out)
-        self._sync_stream()
-        nrng_normal_polar2(self.h, ptr, n, mu, sigma)
-        return out
+        return self._call("P2", n, mu, sigma, out)
 
     def normal_ratio(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
         """Algorithm R (the ratio method): one normal per accepted candidate."""
-        out, ptr, n = self._out(n, out)
-        self._sync_stream()
-        nrng_normal_ratio(self.h, ptr, n, mu, sigma)
-        return out
+        return self._call("R", n, mu, sigma, out)
 
     def normal_ratio1(self, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
         """Algorithm R1 (R with the step-2.5 pretests): the same output as normal_ratio."""
-        out, ptr, n = self._out(n, out)
-        self._sync_stream()
-        nrng_normal_ratio1(self.h, ptr, n, mu, sigma)
-        return out
+        return self._call("R1", n, mu, sigma, out)
 
     def normal(self, method: str, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
-        if method == "P":
-            return self.normal_polar(n, mu, sigma, out=out)
-        if method == "P2":
-            return self.normal_polar2(n, mu, sigma, out=out)
-        if method == "R":
-            return self.normal_ratio(n, mu, sigma, out=out)
-        if method == "R1":
-            return self.normal_ratio1(n, mu, sigma, out=out)
-        return self.normal_boxmuller(n, mu, sigma, METHODS[method], out=out)
+        """n deviates of N(mu, sigma^2) by `method` (B1, B2, B3, P, P2, R, R1) into `out` (a new
+        CUDA tensor by default; a CUDA tensor, CPU tensor or numpy array otherwise)."""
+        return self._call(method, n, mu, sigma, out)
 
     def normal_seq(self, method: str, n: int = None, mu: float = 0.0, sigma: float = 1.0, out=None):
         """Next n deviates of the handle's canonical sequence (RANN3-style buffering)."""
