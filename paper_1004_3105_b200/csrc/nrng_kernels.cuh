@@ -423,10 +423,10 @@ template <int NW, bool EP = false>  // EP: the sequential mode's epoch layout (s
 __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + (threadIdx.x >> 5), threadIdx.x & 31);
+    uint64_t* const buf = smem + warp * (kTriAlloc + kTriScratch);
+    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + warp, lane);
     const Tables tab = load_tables<NW * 32>(reinterpret_cast<double2*>(smem + NW * (kTriAlloc + kTriScratch)));
     __syncthreads();
-    uint64_t* const buf = smem + warp * (kTriAlloc + kTriScratch);
     double* const scr = reinterpret_cast<double*>(buf + kTriAlloc);
     const unsigned lt = lanemask_lt(lane);
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
@@ -487,12 +487,10 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         const uint32_t nw = used < (uint64_t)kLagR ? (uint32_t)used : (uint32_t)kLagR;
         const uint32_t pos0 = (uint32_t)((used - nw) % kTriWin);  // used - nw >= 0
         const uint32_t slot0 = (uint32_t)((C2 + used - nw) % kLagR);
-        for (uint32_t j = lane; j < nw; j += 32) {
-            uint32_t pp = pos0 + j, q = slot0 + j;
-            pp = pp >= (uint32_t)kTriWin ? pp - kTriWin : pp;
-            q = q >= (uint32_t)kLagR ? q - kLagR : q;
-            rk2[q] = NRNG_LD(&buf[pp]);
-        }
+        store_state(rk2, slot0, nw, lane, [&](uint32_t j) {
+            uint32_t pp = pos0 + j;
+            return &buf[pp >= (uint32_t)kTriWin ? pp - kTriWin : pp];
+        });
         NRNG_SYNCWARP();  // every lane has read count[k] before lane 0 updates it
         if (lane == 0) p.count[k] = C2 + used;
         NRNG_SYNCWARP();
@@ -1087,10 +1085,10 @@ template <int M, int NW, bool EP = false>
 __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + (threadIdx.x >> 5), threadIdx.x & 31);
+    uint64_t* const buf = smem + warp * kWinAlloc;
+    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + warp, lane);
     const Tables tab = load_tables<NW * 32>(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
     __syncthreads();
-    uint64_t* const buf = smem + warp * kWinAlloc;
     const PwLane ol = pw_lane(lane);
     const PwPtrs pp = pw_ptrs(buf, ol, lane);
     const unsigned lt = lanemask_lt(lane);
@@ -1219,11 +1217,7 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
         const uint32_t nw = used < (uint64_t)kLagR ? (uint32_t)used : (uint32_t)kLagR;
         const uint32_t pos0 = (uint32_t)((used - nw) & kWinMask);
         const uint32_t slot0 = (uint32_t)((C + used - nw) % kLagR);
-        for (uint32_t j = lane; j < nw; j += 32) {
-            uint32_t q = slot0 + j;
-            q = q >= (uint32_t)kLagR ? q - kLagR : q;
-            rk[q] = NRNG_LD(&buf[swz((pos0 + j) & kWinMask)]);
-        }
+        store_state(rk, slot0, nw, lane, [&](uint32_t j) { return &buf[swz((pos0 + j) & kWinMask)]; });
         if (lane == 0) p.count[k] = C + used;
         NRNG_SYNCWARP();
     }

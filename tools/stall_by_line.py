@@ -1,6 +1,9 @@
 """Warp-stall samples per CUDA source line (and stall reason) for one kernel of an ncu capture.
 
-    python tools/stall_by_line.py PROF.ncu-rep KERNEL_REGEX MANGLED_NAME
+    python tools/stall_by_line.py PROF.ncu-rep KERNEL_REGEX MANGLED_NAME [LIB]
+
+LIB: the libnrng.so build that was profiled (default: the in-tree one) -- its line table maps
+the capture's SASS addresses to source lines.
 """
 import collections
 import csv
@@ -14,8 +17,8 @@ import tempfile
 rep, kre, mangled = sys.argv[1:4]
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tmp = tempfile.mkdtemp()
-subprocess.run(["cuobjdump", "-xelf", "all", os.path.join(root, "paper_1004_3105_b200", "libnrng.so")], cwd=tmp,
-               capture_output=True)
+lib = os.path.abspath(sys.argv[4]) if len(sys.argv) > 4 else os.path.join(root, "paper_1004_3105_b200", "libnrng.so")
+subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, capture_output=True)
 cubin = [os.path.join(tmp, f) for f in os.listdir(tmp) if f.endswith(".cubin")][0]
 dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
 func, line, addr2line = None, None, {}
