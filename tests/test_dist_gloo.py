@@ -157,3 +157,27 @@ def test_cross_rank_lag_sums_brute_force():
         m = min(lags, 37)
         cross = D.cross_rank_lag_sums(a[a.size - m:], b[:lags], lags)
         assert np.allclose(sep + cross, full, rtol=1e-13, atol=1e-12)
+
+
+def test_bench_relaunches_itself_under_torchrun(monkeypatch):
+    # `python bench.py --gpus N` without a launcher re-executes under torch.distributed.run with
+    # N ranks on 127.0.0.1 (the flag used to be ignored outside torchrun)
+    import subprocess
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    seen = {}
+
+    def fake_call(cmd):
+        seen["cmd"] = cmd
+        return 0
+
+    monkeypatch.setattr(subprocess, "call", fake_call)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    assert bench.relaunch(4) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert cmd[cmd.index("--nproc-per-node") + 1] == "4" and cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-4:] == ["--gpus", "4", "--steps", "3"] and cmd[-5].endswith("bench.py")
