@@ -461,15 +461,17 @@ def main():
         ns = int(min(CFG.streams, max(256, 256 * 10.0 / max(csecs, 1e-3))))
         ns = min(CFG.streams, 1 << int(round(math.log2(ns))))
         cv, cper, cn, csecs = oracle_sample(ns, threads)
-        # and once on a single thread: 16 streams x 2^14 pairs per method
-        v1, cper1, cn1, csecs1 = oracle_sample(16, 1)
+        # and once on a single thread, sized for ~5 s: 2^k streams x 2^14 pairs per method
+        _, _, _, s1 = oracle_sample(16, 1)
+        ns1 = min(CFG.streams, 1 << max(4, int(round(math.log2(16 * 5.0 / max(s1, 1e-3))))))
+        v1, cper1, cn1, csecs1 = oracle_sample(ns1, 1)
         cpu = {"value": cv, "unit": "normals/s", "cores": threads, "kind": "oracle",
                "sample": "%d streams x 2^14 pairs per method (B1,B2,B3,P) = %d normals per method, %.1f s wall"
                          % (ns, cn, csecs),
                "per_method": cper, "cpu": cpu_model(),
                "single_thread": {"value": v1, "unit": "normals/s", "cores": 1, "per_method": cper1,
-                                 "sample": "16 streams x 2^14 pairs per method = %d normals per method, %.1f s wall"
-                                           % (cn1, csecs1)}}
+                                 "sample": "%d streams x 2^14 pairs per method = %d normals per method, %.1f s wall"
+                                           % (ns1, cn1, csecs1)}}
 
     line = {
         "metric": METRIC, "value": value, "unit": "normals/s", "n_gpus": world, "steps": args.steps,

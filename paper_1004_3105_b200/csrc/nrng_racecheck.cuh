@@ -6,17 +6,20 @@
 // words other lanes wrote, ordered only by __syncwarp().  compute-sanitizer (racecheck /
 // synccheck) is closed on this GPU pool, so the debug build checks the same property itself.
 //
-// Model: every lane counts the __syncwarp()s it has passed (its epoch; all lanes of a warp
-// pass the same ones).  Two accesses to one 8-byte shared word by different lanes of a warp,
-// at least one a write, race unless a __syncwarp() separates them, i.e. unless they happen in
-// different epochs.  Every instrumented access checks and records, in global shadow arrays
-// indexed by (block, shared word):
-//   W[word] = (epoch + 1) << 32 | writer lane       (last write)
-//   R[word] = (epoch + 1) << 32 | mask of reader lanes in that epoch
-//   load  by lane L in epoch e: RAW race if W's epoch is e and its lane is not L;
-//   store by lane L in epoch e: WAW race if W's epoch is e and its lane is not L,
-//                               WAR race if R's epoch is e and another lane read.
-// Races are counted; the first one's source line, kind and lanes are kept
+// Model: every thread counts the barriers it has passed -- __syncwarp() (NRNG_SYNCWARP) and
+// __syncthreads() (NRNG_SYNCTHREADS) -- its epoch.  The warps of a block pass the same
+// __syncthreads(), the lanes of a warp the same __syncwarp(), and a word is shared either within
+// one warp (the windows and scratch of the warp-per-stream kernels) or, in coop_kernel, by the
+// block with only __syncthreads() ordering it, so the accessors of one word always have
+// comparable epochs.  Two accesses to one 8-byte shared word by different threads, at least one
+// a write, race unless a barrier separates them, i.e. unless their epochs differ.  Every
+// instrumented access checks and records, in global shadow arrays indexed by (block, shared word):
+//   W[word] = (epoch + 1) << 32 | writer thread                       (last write)
+//   R[word] = (epoch + 1) << 32 | several-readers flag << 16 | reader (reads in that epoch)
+//   load  by thread t in epoch e: RAW race if W's epoch is e and its writer is not t;
+//   store by thread t in epoch e: WAW race if W's epoch is e and its writer is not t,
+//                                 WAR race if R's epoch is e and a thread other than t read.
+// Races are counted; the first one's source line, kind and threads are kept
 // (nrng_racecheck_result).  The shadows and epochs are cleared before every launch.
 #pragma once
 #include <cstdint>
@@ -35,7 +38,7 @@ struct RcState {
     unsigned long long* w;      // kRcMaxBlocks x kRcShadowWords
     unsigned long long* r;      // kRcMaxBlocks x kRcShadowWords
     uint32_t* epoch;            // per thread (block-major)
-    unsigned long long* races;  // [0] count, [1] first race: line << 32 | kind << 16 | lane << 8 | other lane
+    unsigned long long* races;  // [0] count, [1] first race: line << 32 | kind << 24 | thread << 12 | other
     unsigned long long* checks; // accesses checked
 };
 __device__ RcState g_rc;
@@ -43,30 +46,32 @@ __device__ RcState g_rc;
 __device__ __forceinline__ uint32_t rc_tid() {
     return (blockIdx.x % kRcMaxBlocks) * blockDim.x + threadIdx.x;
 }
-__device__ __forceinline__ void rc_report(uint32_t line, uint32_t kind, uint32_t lane, uint32_t other) {
+__device__ __forceinline__ void rc_report(uint32_t line, uint32_t kind, uint32_t me, uint32_t other) {
     const unsigned long long n = atomicAdd(&g_rc.races[0], 1ull);
     if (n == 0)
-        atomicExch(&g_rc.races[1], ((unsigned long long)line << 32) | (kind << 16) | (lane << 8) | other);
+        atomicExch(&g_rc.races[1], ((unsigned long long)line << 32) | (kind << 24) | ((me & 0xfff) << 12) |
+                                       (other & 0xfff));
 }
-// kind: 1 RAW, 2 WAW, 3 WAR
+// kind: 1 RAW, 2 WAW, 3 WAR; threads are threadIdx.x (lane + 32 warp)
 __device__ __forceinline__ void rc_access(const void* p, bool store, uint32_t line) {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
     const uint64_t slot = (uint64_t)(blockIdx.x % kRcMaxBlocks) * kRcShadowWords + (a >> 3);
-    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t me = threadIdx.x;
     const unsigned long long e = (unsigned long long)g_rc.epoch[rc_tid()] + 1;
     atomicAdd(&g_rc.checks[0], 1ull);
     if (store) {
-        const unsigned long long w = atomicExch(&g_rc.w[slot], (e << 32) | lane);
-        if ((w >> 32) == e && (uint32_t)(w & 0xff) != lane) rc_report(line, 2, lane, (uint32_t)(w & 0xff));
+        const unsigned long long w = atomicExch(&g_rc.w[slot], (e << 32) | me);
+        if ((w >> 32) == e && (uint32_t)(w & 0xffff) != me) rc_report(line, 2, me, (uint32_t)(w & 0xffff));
         const unsigned long long r = atomicAdd(&g_rc.r[slot], 0ull);
-        if ((r >> 32) == e && ((uint32_t)r & ~(1u << lane)) != 0)
-            rc_report(line, 3, lane, __ffs((uint32_t)r & ~(1u << lane)) - 1);
+        if ((r >> 32) == e && (((r >> 16) & 1) || (uint32_t)(r & 0xffff) != me))
+            rc_report(line, 3, me, (uint32_t)(r & 0xffff));
     } else {
         const unsigned long long w = atomicAdd(&g_rc.w[slot], 0ull);
-        if ((w >> 32) == e && (uint32_t)(w & 0xff) != lane) rc_report(line, 1, lane, (uint32_t)(w & 0xff));
+        if ((w >> 32) == e && (uint32_t)(w & 0xffff) != me) rc_report(line, 1, me, (uint32_t)(w & 0xffff));
         unsigned long long old = atomicAdd(&g_rc.r[slot], 0ull);
-        for (;;) {  // merge this lane into the epoch's reader mask (or start the epoch's mask)
-            const unsigned long long nw = ((old >> 32) == e) ? (old | (1ull << lane)) : ((e << 32) | (1ull << lane));
+        for (;;) {  // this epoch's first reader, or mark the word read by several threads
+            const unsigned long long nw = ((old >> 32) != e) ? ((e << 32) | me)
+                                          : ((uint32_t)(old & 0xffff) == me ? old : (old | (1ull << 16)));
             if (nw == old) break;
             const unsigned long long prev = atomicCAS(&g_rc.r[slot], old, nw);
             if (prev == old) break;
@@ -88,13 +93,19 @@ __device__ __forceinline__ void rc_sync() {
     __syncwarp();
     g_rc.epoch[rc_tid()] += 1;
 }
+__device__ __forceinline__ void rc_syncthreads() {
+    __syncthreads();
+    g_rc.epoch[rc_tid()] += 1;
+}
 #define NRNG_LD(p) ::nrng::rc_ld((p), __LINE__)
 #define NRNG_ST(p, v) ::nrng::rc_st((p), (v), __LINE__)
 #define NRNG_SYNCWARP() ::nrng::rc_sync()
+#define NRNG_SYNCTHREADS() ::nrng::rc_syncthreads()
 #else
 #define NRNG_LD(p) (*(p))
 #define NRNG_ST(p, v) (*(p) = (v))
 #define NRNG_SYNCWARP() __syncwarp()
+#define NRNG_SYNCTHREADS() __syncthreads()
 #endif
 
 }  // namespace nrng

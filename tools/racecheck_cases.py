@@ -30,8 +30,8 @@ def report(name):
     total_checks += checks
     desc = ""
     if races:
-        desc = " first: line %d %s lane %d vs lane %d" % (first >> 32, KIND.get((first >> 16) & 0xff, "?"),
-                                                           (first >> 8) & 0xff, first & 0xff)
+        desc = " first: line %d %s thread %d vs thread %d" % (first >> 32, KIND.get((first >> 24) & 0xff, "?"),
+                                                               (first >> 12) & 0xfff, first & 0xfff)
     rows.append("%-44s checks %12d  races %d%s" % (name, checks, races, desc))
     print(rows[-1], flush=True)
 
@@ -69,7 +69,11 @@ def main():
         report("%s S=3000 misaligned (bm/polar 20-warp)" % m)
         g = P.Generator(8, 600)
         run(g, m, per * 600 * 300 + 1)
-        report("%s S=600 x 300 (4-warp blocks)" % m)
+        report("%s S=600 x 300 (4-warp blocks; B1/B2: coop_kernel<V,4>)" % m)
+        if m in ("B1", "B2"):
+            g = P.Generator(8, 1700)
+            run(g, m, per * 1700 * 300 + 1)
+            report("%s S=1700 x 300 (coop_kernel<V,2> / 4-warp blocks)" % m)
         run(g, m, per * 600 * 140, misaligned=True)
         report("%s S=600 misaligned (bm/polar 4-warp)" % m)
         g = P.Generator(9, 512)
