@@ -72,7 +72,6 @@ void rc_reset(cudaStream_t) {}
 
 struct Occ {
     int bm[4] = {0, 0, 0, 0}, pw[3] = {0, 0, 0}, tri = 0, polar = 0, ratio = 0, ratio1 = 0, uni = 0, mask = 0, init = 0;  // 4-warp-block kernels
-    int coop4[3] = {0, 0, 0}, coop2[3] = {0, 0, 0};  // coop_kernel<V, W> blocks per SM
 };
 
 }  // namespace
@@ -143,9 +142,6 @@ uint64_t eff_qmax(const BulkParams& p) {
     return std::min(qmax > p.jb ? qmax - p.jb : 0, p.jcap);
 }
 
-#ifndef NRNG_COOP
-#define NRNG_COOP 1
-#endif
 #ifndef NRNG_PW_SMALL
 #define NRNG_PW_SMALL 1
 #endif
@@ -174,17 +170,6 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
             pw_kernel<V, kPwWarps><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
             return;
         }
-#if NRNG_COOP
-        // few streams: W warps per stream while the whole call fits one wave of such blocks
-        if (plain && ns <= (uint32_t)(h->occ.coop4[V] * h->num_sms)) {
-            coop_kernel<V, 4><<<ns, 4 * 32, coop_smem(), st>>>(p);
-            return;
-        }
-        if (plain && ns <= (uint32_t)(h->occ.coop2[V] * h->num_sms)) {
-            coop_kernel<V, 2><<<ns, 2 * 32, coop_smem(), st>>>(p);
-            return;
-        }
-#endif
         if (NRNG_PW_SMALL && plain) {  // fewer streams than one-block-per-SM slots: 4-warp blocks
             pw_kernel<V, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.pw[V], h->num_sms),
                                            kWarpsPerBlock * 32, bm_smem(kWarpsPerBlock), st>>>(p);
@@ -447,10 +432,6 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     h->occ.tri = occupancy(b3_kernel<kWarpsPerBlock>, kWarpsPerBlock, tri_smem(kWarpsPerBlock));
     h->occ.pw[1] = occupancy(pw_kernel<1, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
     h->occ.pw[2] = occupancy(pw_kernel<2, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
-    h->occ.coop4[1] = occupancy(coop_kernel<1, 4>, 4, coop_smem());
-    h->occ.coop4[2] = occupancy(coop_kernel<2, 4>, 4, coop_smem());
-    h->occ.coop2[1] = occupancy(coop_kernel<1, 2>, 2, coop_smem());
-    h->occ.coop2[2] = occupancy(coop_kernel<2, 2>, 2, coop_smem());
     occupancy(pw_kernel<7, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
     h->occ.ratio1 = occupancy(pw_kernel<7, kWarpsPerBlock>, kWarpsPerBlock, r1_smem(kWarpsPerBlock));
     occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));

@@ -1223,91 +1223,6 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     }
 }
 
-// ------------------------------------------------------------------ few streams, W warps each
-// Box-Muller calls with fewer streams than the GPU has warp slots (C1: 1024 streams x 512 pairs)
-// leave pw_kernel's warp-per-stream chains latency-bound (~7 warps per SM).  Here the W warps of a
-// block share one stream: the rows of a 4-row block are independent (4 x 64 < 273), so warp w
-// generates rows w, w + W, ... of each block (the pair-window generator at run-time positions,
-// no mirror) and transforms them (R = 4 / W pairs per lane); a block barrier separates blocks
-// (block b+1 reads block b at lag 273 and overwrites what block b read at lag 607).  The state is
-// loaded and written back by all W x 32 threads.  Window: 1024 words per block (8 KB) + the table.
-template <int M, int W>
-__global__ void __launch_bounds__(W * 32) coop_kernel(BulkParams p) {
-    static_assert(M == 1 || M == 2, "Box-Muller B1/B2");
-    static_assert(W == 2 || W == 4, "rows of a block split evenly");
-    constexpr int R = 4 / W;
-    extern __shared__ __align__(16) uint64_t smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-    uint64_t* const buf = smem;
-    if (warp == 0) prefetch_first_state(p, p.s_begin + blockIdx.x, lane);
-    const Tables tab = load_tables<W * 32>(reinterpret_cast<double2*>(smem + kWin));
-    NRNG_SYNCTHREADS();
-    const PwLane ol = pw_lane(lane);
-    for (uint32_t k = p.s_begin + blockIdx.x; k < p.s_end; k += gridDim.x) {
-        const Quota qk = quota(p, k);  // block-uniform
-        if (qk.cnt == 0) continue;
-        const uint64_t C = p.count[k];
-        uint64_t* rk = p.ring + (uint64_t)k * kPitch;
-        {   // x_{C-607+j} -> logical position 417 + j, all W x 32 threads
-            constexpr int T = (kLagR + 32 * W - 1) / (32 * W);
-            const uint32_t base = (uint32_t)(C % kLagR);
-            uint64_t v[T];
-#pragma unroll
-            for (int t = 0; t < T; ++t) {
-                const uint32_t j = tid + 32 * W * t;
-                if (j < (uint32_t)kLagR) {
-                    uint32_t q = base + j;
-                    q = q >= (uint32_t)kLagR ? q - kLagR : q;
-                    v[t] = rk[q];
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < T; ++t) {
-                const uint32_t j = tid + 32 * W * t;
-                if (j < (uint32_t)kLagR) NRNG_ST(&buf[swz((kWin - kLagR) + j)], v[t]);
-            }
-        }
-        NRNG_SYNCTHREADS();
-        if (warp == 0) prefetch_state<2>(p, k + gridDim.x, lane);
-        const uint64_t nrows = (qk.cnt + 31) / 32;  // row r = pairs 32 r .. 32 r + 31, at logical 64 r
-        for (uint64_t r0 = 0; r0 < nrows; r0 += 4) {
-            uint64_t wu[R], wv[R];
-#pragma unroll
-            for (int t = 0; t < R; ++t) {
-                const uint64_t r = r0 + warp + W * t;
-                uint64_t a[1], b[1];
-                if (r < nrows) pw_gen<1, true>(buf, (uint32_t)(64 * r) & kWinMask, ol, a, b, lane);
-                wu[t] = a[0];
-                wv[t] = b[0];
-            }
-            double x[R], y[R];
-            if (M == 1)
-                b1_pairs<R>(wu, wv, p.tp, tab, x, y);
-            else
-                b2_pairs<R>(wu, wv, p.tp, tab, x, y);
-#pragma unroll
-            for (int t = 0; t < R; ++t) {
-                const uint64_t j = 32 * (r0 + warp + W * t) + lane;  // pair index in the stream
-                if (j < qk.cnt) store_pair(p.out, 2 * (qk.off + j), p.shift, p.n, x[t], y[t], p.aligned);
-            }
-            NRNG_SYNCTHREADS();
-        }
-        // write back the last min(used, 607) consumed words (word i at logical i mod 1024)
-        const uint64_t used = 2 * qk.cnt;
-        const uint32_t nw = used < (uint64_t)kLagR ? (uint32_t)used : (uint32_t)kLagR;
-        const uint32_t pos0 = (uint32_t)((used - nw) & kWinMask);
-        const uint32_t slot0 = (uint32_t)((C + used - nw) % kLagR);
-        for (uint32_t j = tid; j < nw; j += 32 * W) {
-            uint32_t q = slot0 + j;
-            q = q >= (uint32_t)kLagR ? q - kLagR : q;
-            rk[q] = NRNG_LD(&buf[swz((pos0 + j) & kWinMask)]);
-        }
-        if (tid == 0) p.count[k] = C + used;
-        NRNG_SYNCTHREADS();  // the window is reused by the next stream
-    }
-}
-constexpr size_t coop_smem() { return (size_t)kWin * sizeof(uint64_t) + kTabBytes; }
-
 // ------------------------------------------------------------------ tiny quotas
 // Calls that give every stream only a few pairs (the C4 sweep: n <= 2^22 over 2^16 streams
 // gives 1-32 pairs per stream) are bound by per-stream latency and state traffic, not

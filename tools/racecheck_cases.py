@@ -69,11 +69,7 @@ def main():
         report("%s S=3000 misaligned (bm/polar 20-warp)" % m)
         g = P.Generator(8, 600)
         run(g, m, per * 600 * 300 + 1)
-        report("%s S=600 x 300 (4-warp blocks; B1/B2: coop_kernel<V,4>)" % m)
-        if m in ("B1", "B2"):
-            g = P.Generator(8, 1700)
-            run(g, m, per * 1700 * 300 + 1)
-            report("%s S=1700 x 300 (coop_kernel<V,2> / 4-warp blocks)" % m)
+        report("%s S=600 x 300 (4-warp blocks)" % m)
         run(g, m, per * 600 * 140, misaligned=True)
         report("%s S=600 misaligned (bm/polar 4-warp)" % m)
         g = P.Generator(9, 512)
