@@ -433,10 +433,9 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
         prefetch_state<1>(p, k + gridDim.x * NW, lane);
-        const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         // x_{C-607+j} -> position 1152 - 607 + j
-        load_state(rk, C, lane, [&](uint32_t j) { return buf + (kTriWin - kLagR) + j; }, all_state_words);
+        const uint64_t C = load_state_rot(rk, p.count + k, lane, [&](uint32_t j) { return buf + (kTriWin - kLagR) + j; });
         NRNG_SYNCWARP();
         prefetch_state<2>(p, k + gridDim.x * NW, lane);
         // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
@@ -1097,10 +1096,17 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
         const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
         if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<1>(p, k + gridDim.x * NW, lane);
-        const uint64_t C = p.count[k];
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
-        // x_{C-607+j} -> logical position 417 + j
-        load_state(rk, C, lane, [&](uint32_t j) { return buf + swz((kWin - kLagR) + j); }, all_state_words);
+        // x_{C-607+j} -> logical position 417 + j.  (Ring and counter loaded together; except in
+        // B1's one-block-per-SM kernel, whose schedule came out 4% slower with it: measured.)
+        auto win = [&](uint32_t j) { return buf + swz((kWin - kLagR) + j); };
+        uint64_t C;
+        if constexpr (M == 1 && NW == kPwWarps) {
+            C = p.count[k];
+            load_state(rk, C, lane, win, all_state_words);
+        } else {
+            C = load_state_rot(rk, p.count + k, lane, win);
+        }
         NRNG_SYNCWARP();
         if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<2>(p, k + gridDim.x * NW, lane);
         uint64_t used;  // words consumed by this call

@@ -9,8 +9,8 @@
 // Model: every thread counts the barriers it has passed -- __syncwarp() (NRNG_SYNCWARP) and
 // __syncthreads() (NRNG_SYNCTHREADS) -- its epoch.  The warps of a block pass the same
 // __syncthreads(), the lanes of a warp the same __syncwarp(), and a word is shared either within
-// one warp (the windows and scratch of the warp-per-stream kernels) or, in coop_kernel, by the
-// block with only __syncthreads() ordering it, so the accessors of one word always have
+// one warp (the windows and scratch of the warp-per-stream kernels) or by a block with only
+// __syncthreads() ordering it (NRNG_SYNCTHREADS), so the accessors of one word always have
 // comparable epochs.  Two accesses to one 8-byte shared word by different threads, at least one
 // a write, race unless a barrier separates them, i.e. unless their epochs differ.  Every
 // instrumented access checks and records, in global shadow arrays indexed by (block, shared word):

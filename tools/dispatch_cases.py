@@ -1,8 +1,9 @@
-"""Small calls that reach every kernel nrng.cu launches, for compute-sanitizer (racecheck /
-synccheck / memcheck, one tool per GPU call) and for the ncu launch list of the dispatch paths.
+"""Small calls that reach every kernel nrng.cu launches: the ncu launch list of the dispatch
+paths (tools/round_snapshot.sh; profiles/<tag>_dispatch_launches.txt).  (compute-sanitizer, which
+it was first written for, is closed on this GPU pool: tools/racecheck_cases.py runs the same paths
+on the library's own race-detector build.)
 
-    python tools/sanitize_cases.py            # plain run first (must exit 0)
-    compute-sanitizer --tool racecheck python tools/sanitize_cases.py
+    python tools/dispatch_cases.py
 
 Shapes (DESIGN.md §6 dispatch): >= 16 x 148 streams with > 128 pairs per stream: the
 one-block-per-SM pw_kernel<M,16> / b3_kernel<16>; fewer streams: pw_kernel<M,4> / b3_kernel<4>
