@@ -1278,7 +1278,7 @@ __device__ __forceinline__ void ring_commit(uint64_t* __restrict__ r, uint32_t& 
 template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2; 6 = R (units: normals, one per accept)
 __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
     __shared__ double2 tabs[kTabBytes / 16];
-    const Tables tab = load_tables<kTinyThreads>(tabs);
+    const Tables tab = load_tables_single<kTinyThreads>(tabs);
     __syncthreads();
     const uint32_t k = p.s_begin + blockIdx.x * kTinyThreads + threadIdx.x;
     if (k >= p.s_end) return;
@@ -1394,14 +1394,28 @@ constexpr uint64_t kMidMinPairs = NRNG_MID_MIN, kMidMaxPairs = NRNG_MID_MAX;  //
 template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2; 6 = R (units: normals, one per accept)
 __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
     __shared__ double2 tabs[kTabBytes / 16];
-    const Tables tab = load_tables<kMidWarps * 32>(tabs);
-    __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t k0 = p.s_begin + blockIdx.x * kMidWarps + warp, stride = gridDim.x * kMidWarps;
+    // the counters of the warp's next 32 streams, one per lane (a stream's ring reads need its
+    // counter: loading them a batch ahead leaves one memory latency per stream, not two); the
+    // first batch is in flight while the block loads its ln table
+    auto counters = [&](uint32_t kb) {
+        const uint64_t kk = kb + (uint64_t)lane * stride;
+        return kk < p.s_end ? p.count[kk] : 0ull;
+    };
+    uint64_t cbatch = counters(k0);
+    const Tables tab = load_tables_single<kMidWarps * 32>(tabs);
+    __syncthreads();
     const unsigned lt = lanemask_lt(lane);
-    for (uint32_t k = p.s_begin + blockIdx.x * kMidWarps + warp; k < p.s_end; k += gridDim.x * kMidWarps) {
+    uint32_t i = 0;
+    for (uint32_t k = k0; k < p.s_end; k += stride, ++i) {
+        if (i == 32) {
+            cbatch = counters(k);
+            i = 0;
+        }
         const Quota qk = quota(p, k);
         if (qk.cnt == 0) continue;
-        const uint64_t C = p.count[k];
+        const uint64_t C = __shfl_sync(kFull, cbatch, i);
         uint64_t* r = p.ring + (uint64_t)k * kPitch;
         const uint32_t c0 = (uint32_t)(C % kLagR);
         uint32_t i0 = 0;  // words of the call consumed before this step
