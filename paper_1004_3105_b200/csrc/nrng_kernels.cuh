@@ -1278,7 +1278,7 @@ __device__ __forceinline__ void ring_commit(uint64_t* __restrict__ r, uint32_t& 
 template <int V>  // 1, 2, 3 = B1, B2, B3; 4 = Polar; 5 = P2; 6 = R (units: normals, one per accept)
 __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(BulkParams p) {
     __shared__ double2 tabs[kTabBytes / 16];
-    const Tables tab = load_tables_single<kTinyThreads>(tabs);
+    const Tables tab = load_tables<kTinyThreads>(tabs);
     __syncthreads();
     const uint32_t k = p.s_begin + blockIdx.x * kTinyThreads + threadIdx.x;
     if (k >= p.s_end) return;
@@ -1404,7 +1404,7 @@ __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
         return kk < p.s_end ? p.count[kk] : 0ull;
     };
     uint64_t cbatch = counters(k0);
-    const Tables tab = load_tables_single<kMidWarps * 32>(tabs);
+    const Tables tab = load_tables<kMidWarps * 32>(tabs);
     __syncthreads();
     const unsigned lt = lanemask_lt(lane);
     uint32_t i = 0;
