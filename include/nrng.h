@@ -34,11 +34,15 @@
  * Memory and ownership
  *   A handle owns its device state (S x 608 u64 ring + S u64 counters) on the device
  *   current at create time.  `out` for the normal/uniform calls may be a DEVICE pointer
- *   (the fast path: one kernel launch, asynchronous on the handle's stream) or a HOST
- *   pointer (pinned or pageable: generated in stream-range chunks into handle-owned
- *   device staging buffers and copied back, overlapped; the call returns after the
+ *   (the fast path: asynchronous on the handle's stream; one kernel launch, or one per
+ *   2^28 units of a stream's quota when a stream's quota is longer) or a HOST pointer
+ *   (pinned or pageable: generated into two handle-owned 128 MiB device staging buffers
+ *   -- ranges of whole streams, or pieces of one stream when its output exceeds a staging
+ *   buffer -- and copied back overlapped with the next piece; the call returns after the
  *   host data is complete).  Device outputs should be 16-byte aligned (8-byte aligned
- *   is accepted on a slower store path).  No call allocates host memory for outputs.
+ *   is accepted on a slower store path).  `out` must hold n doubles; the library cannot
+ *   check it (the Python binding checks dtype, contiguity and device).  No call
+ *   allocates host memory for outputs.
  *
  * Errors: functions return NRNG_OK (0) or a negative code; the same code is kept as a
  * thread-local "last error" (nrng_last_error).  Argument errors are detected before
@@ -147,7 +151,9 @@ int nrng_stream_counts(nrng_handle h, uint64_t* host_counts);
 /* Copy the full state to host: ring S x 607 u64 (x_n at [k][n mod 607]) and counters.
  * Either pointer may be NULL.  Synchronises. */
 int nrng_get_state(nrng_handle h, uint64_t* host_ring, uint64_t* host_counts);
-/* Restore a state produced by nrng_get_state (same S). */
+/* Restore a state produced by nrng_get_state (same S); either pointer may be NULL.  Any
+ * deviates the sequential mode still buffers are discarded (they came from the old state).
+ * Synchronises. */
 int nrng_set_state(nrng_handle h, const uint64_t* host_ring, const uint64_t* host_counts);
 /* Block until all work enqueued by the handle has completed. */
 int nrng_synchronize(nrng_handle h);
