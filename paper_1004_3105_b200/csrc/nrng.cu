@@ -37,7 +37,7 @@ constexpr size_t bm_smem(int nw) { return win_bytes(nw) + kTabBytes; }
 constexpr size_t r1_smem(int nw) { return bm_smem(nw) + (size_t)nw * 32 * sizeof(double); }  // + R1 scratch
 constexpr size_t polar_smem(int nw) { return win_bytes(nw) + kTabBytes + (size_t)nw * 32 * sizeof(double); }  // + P2 tail scratch
 constexpr size_t kMaxSmem = 227 * 1024;  // per block, sm_100a opt-in maximum
-static_assert(bm_smem(kPwWarps) <= kMaxSmem && r1_smem(kPwWarps) <= kMaxSmem && tri_smem(kTriWarps) <= kMaxSmem &&
+static_assert(bm_smem(kPwWarps) <= kMaxSmem && pw_smem(5, false, kPwWarps) <= kMaxSmem && pw_smem(7, false, kPwWarps) <= kMaxSmem && r1_smem(kPwWarps) <= kMaxSmem && tri_smem(kTriWarps) <= kMaxSmem &&
                   bm_smem(kBigBlock) <= kMaxSmem && polar_smem(kBigBlockPolar) <= kMaxSmem,
               "one-block-per-SM kernels must fit the shared memory of an SM");
 constexpr size_t kUniSmem = win_bytes(kWarpsPerBlock);
@@ -167,12 +167,12 @@ void launch_bm(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t st)
         }
     } else {
         if (plain && ns >= (uint32_t)(kPwWarps * h->num_sms)) {
-            pw_kernel<V, kPwWarps><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
+            pw_kernel<V, kPwWarps><<<h->num_sms, kPwWarps * 32, pw_smem(V, false, kPwWarps), st>>>(p);
             return;
         }
         if (NRNG_PW_SMALL && plain) {  // fewer streams than one-block-per-SM slots: 4-warp blocks
             pw_kernel<V, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.pw[V], h->num_sms),
-                                           kWarpsPerBlock * 32, bm_smem(kWarpsPerBlock), st>>>(p);
+                                           kWarpsPerBlock * 32, pw_smem(V, false, kWarpsPerBlock), st>>>(p);
             return;
         }
     }
@@ -199,12 +199,12 @@ void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t 
     }
     if ((M == 1 || NRNG_P2_PW) && p.aligned && p.log2E == 0 && eff_qmax(p) < (1ull << 31) &&
         ns >= (uint32_t)(kPwWarps * h->num_sms))
-        pw_kernel<kPw, kPwWarps><<<h->num_sms, kPwWarps * 32, kPw == 5 ? r1_smem(kPwWarps) : bm_smem(kPwWarps), st>>>(p);
+        pw_kernel<kPw, kPwWarps><<<h->num_sms, kPwWarps * 32, pw_smem(kPw, false, kPwWarps), st>>>(p);
     else if (ns >= (uint32_t)(kBigBlockPolar * h->num_sms))
         polar_kernel<kBigBlockPolar, M><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
     else if (M == 1 && NRNG_PW_SMALL && p.aligned && p.log2E == 0 && eff_qmax(p) < (1ull << 31))
         pw_kernel<4, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.pw[0], h->num_sms), kWarpsPerBlock * 32,
-                                       bm_smem(kWarpsPerBlock), st>>>(p);
+                                       pw_smem(4, false, kWarpsPerBlock), st>>>(p);
     else
         polar_kernel<kWarpsPerBlock, M><<<grid_for(ns, kWarpsPerBlock, h->occ.polar, h->num_sms),
                                           kWarpsPerBlock * 32, polar_smem(kWarpsPerBlock), st>>>(p);
@@ -250,17 +250,17 @@ cudaError_t launch_bulk(nrng_handle h, Kind kind, BulkParams p, cudaStream_t st)
         case Kind::POLAR2: launch_polar<2>(h, p, ns, st); break;
         case Kind::RATIO:
             if (ns >= (uint32_t)(kPwWarps * h->num_sms))
-                pw_kernel<6, kPwWarps><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
+                pw_kernel<6, kPwWarps><<<h->num_sms, kPwWarps * 32, pw_smem(6, false, kPwWarps), st>>>(p);
             else
                 pw_kernel<6, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.ratio, h->num_sms),
-                                                kWarpsPerBlock * 32, bm_smem(kWarpsPerBlock), st>>>(p);
+                                                kWarpsPerBlock * 32, pw_smem(6, false, kWarpsPerBlock), st>>>(p);
             break;
         case Kind::RATIO1:
             if (ns >= (uint32_t)(kPwWarps * h->num_sms))
-                pw_kernel<7, kPwWarps><<<h->num_sms, kPwWarps * 32, r1_smem(kPwWarps), st>>>(p);
+                pw_kernel<7, kPwWarps><<<h->num_sms, kPwWarps * 32, pw_smem(7, false, kPwWarps), st>>>(p);
             else
                 pw_kernel<7, kWarpsPerBlock><<<grid_for(ns, kWarpsPerBlock, h->occ.ratio1, h->num_sms),
-                                                kWarpsPerBlock * 32, r1_smem(kWarpsPerBlock), st>>>(p);
+                                                kWarpsPerBlock * 32, pw_smem(7, false, kWarpsPerBlock), st>>>(p);
             break;
         case Kind::UNIFORM:
             uniform_kernel<<<grid_for(ns, kWarpsPerBlock, h->occ.uni, h->num_sms), kWarpsPerBlock * 32, kUniSmem,
@@ -418,22 +418,22 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(bm_kernel<2, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(bm_kernel<3, kBigBlock>, kBigBlock, bm_smem(kBigBlock));
     occupancy(b3_kernel<kTriWarps>, kTriWarps, tri_smem(kTriWarps));
-    occupancy(pw_kernel<1, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
-    occupancy(pw_kernel<2, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
-    occupancy(pw_kernel<4, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
-    occupancy(pw_kernel<5, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
-    occupancy(pw_kernel<6, kPwWarps>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(pw_kernel<1, kPwWarps>, kPwWarps, pw_smem(1, false, kPwWarps));
+    occupancy(pw_kernel<2, kPwWarps>, kPwWarps, pw_smem(2, false, kPwWarps));
+    occupancy(pw_kernel<4, kPwWarps>, kPwWarps, pw_smem(4, false, kPwWarps));
+    occupancy(pw_kernel<5, kPwWarps>, kPwWarps, pw_smem(5, false, kPwWarps));
+    occupancy(pw_kernel<6, kPwWarps>, kPwWarps, pw_smem(6, false, kPwWarps));
     occupancy(pw_kernel<1, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
     occupancy(pw_kernel<2, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
     occupancy(pw_kernel<4, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
     occupancy(b3_kernel<kTriWarps, true>, kTriWarps, tri_smem(kTriWarps));
-    h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
-    h->occ.pw[0] = occupancy(pw_kernel<4, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
+    h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, pw_smem(6, false, kWarpsPerBlock));
+    h->occ.pw[0] = occupancy(pw_kernel<4, kWarpsPerBlock>, kWarpsPerBlock, pw_smem(4, false, kWarpsPerBlock));
     h->occ.tri = occupancy(b3_kernel<kWarpsPerBlock>, kWarpsPerBlock, tri_smem(kWarpsPerBlock));
-    h->occ.pw[1] = occupancy(pw_kernel<1, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
-    h->occ.pw[2] = occupancy(pw_kernel<2, kWarpsPerBlock>, kWarpsPerBlock, bm_smem(kWarpsPerBlock));
-    occupancy(pw_kernel<7, kPwWarps>, kPwWarps, r1_smem(kPwWarps));
-    h->occ.ratio1 = occupancy(pw_kernel<7, kWarpsPerBlock>, kWarpsPerBlock, r1_smem(kWarpsPerBlock));
+    h->occ.pw[1] = occupancy(pw_kernel<1, kWarpsPerBlock>, kWarpsPerBlock, pw_smem(1, false, kWarpsPerBlock));
+    h->occ.pw[2] = occupancy(pw_kernel<2, kWarpsPerBlock>, kWarpsPerBlock, pw_smem(2, false, kWarpsPerBlock));
+    occupancy(pw_kernel<7, kPwWarps>, kPwWarps, pw_smem(7, false, kPwWarps));
+    h->occ.ratio1 = occupancy(pw_kernel<7, kWarpsPerBlock>, kWarpsPerBlock, pw_smem(7, false, kWarpsPerBlock));
     occupancy(polar_kernel<kBigBlockPolar, 1>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     occupancy(polar_kernel<kBigBlockPolar, 2>, kBigBlockPolar, polar_smem(kBigBlockPolar));
     occupancy(polar_kernel<kBigBlockPolar, 2, true>, kBigBlockPolar, polar_smem(kBigBlockPolar));

@@ -53,6 +53,32 @@ __device__ __forceinline__ uint64_t pair_slot(const BulkParams& p, uint64_t off,
 // over all SMs) and NW = kBigBlock warps, one block per SM (the tables are stored once per
 // SM instead of once per 4 warps, which is what lets 20 windows fit in 227 KB).
 constexpr size_t win_bytes(int nw) { return (size_t)nw * kWinAlloc * sizeof(uint64_t); }
+// Algorithm P's pair-window kernel stages the warp's NEXT stream -- its ring row and counter --
+// in shared memory with cp.async while the current one computes: kStageWords after the
+// 1024-word window, in place of the mirror it does not use.  Measured (interleaved, r2y/r2z):
+// C2 (2^14 streams of 512 pairs) 64.3 -> 60.0 us, the bench shape within noise; for B2, P2, R
+// and R1 it cost 1-2% at the bench shape and in C3, so they keep the L2 prefetch.
+#ifndef NRNG_STAGE_NEXT
+#define NRNG_STAGE_NEXT 1
+#endif
+constexpr int kStageWords = kPitch + 2;  // ring row (608) + counter + pad (16-byte multiple)
+__host__ __device__ constexpr bool pw_staged(int M, bool EP) { return NRNG_STAGE_NEXT && M == 4 && !EP; }
+__host__ __device__ constexpr int pw_stride(int M, bool EP) { return pw_staged(M, EP) ? kWin + kStageWords : kWinAlloc; }
+constexpr size_t pw_smem(int M, bool EP, int nw) {
+    return (size_t)nw * pw_stride(M, EP) * sizeof(uint64_t) + kTabBytes +
+           ((M == 5 || M == 7) ? (size_t)nw * 32 * sizeof(double) : 0);
+}
+// Issue the cp.async copies of stream kn's ring row and counter into stg (one commit group).
+__device__ __forceinline__ void stage_state(uint64_t* stg, const BulkParams& p, uint32_t kn, int lane) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(stg);
+    const uint64_t* row = p.ring + (uint64_t)kn * kPitch;
+    for (int c = lane; c < kPitch / 2; c += 32)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s + 16 * c), "l"(row + 2 * c) : "memory");
+    if (lane == 0)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s + 8 * kPitch), "l"(p.count + kn) : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 #ifndef NRNG_BIGBLOCK
 #define NRNG_BIGBLOCK 20
 #endif
@@ -1085,31 +1111,53 @@ template <int M, int NW, bool EP = false>
 __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
     extern __shared__ __align__(16) uint64_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint64_t* const buf = smem + warp * kWinAlloc;
-    prefetch_first_state(p, p.s_begin + blockIdx.x * NW + warp, lane);
-    const Tables tab = load_tables<NW * 32>(reinterpret_cast<double2*>(smem + NW * kWinAlloc));
+    constexpr bool kStaged = pw_staged(M, EP);
+    constexpr int kStride = pw_stride(M, EP);
+    uint64_t* const buf = smem + warp * kStride;
+    uint64_t* const stg = buf + kWin;  // kStaged: the next stream's ring row and counter
+    if constexpr (kStaged) {
+        if (p.s_begin + blockIdx.x * NW + warp < p.s_end) stage_state(stg, p, p.s_begin + blockIdx.x * NW + warp, lane);
+    } else {
+        prefetch_first_state(p, p.s_begin + blockIdx.x * NW + warp, lane);
+    }
+    const Tables tab = load_tables<NW * 32>(reinterpret_cast<double2*>(smem + NW * kStride));
     __syncthreads();
     const PwLane ol = pw_lane(lane);
     const PwPtrs pp = pw_ptrs(buf, ol, lane);
     const unsigned lt = lanemask_lt(lane);
-    double* const scr = reinterpret_cast<double*>(smem + NW * kWinAlloc + kTabBytes / 8) + 32 * warp;  // M = 5, 7
+    double* const scr = reinterpret_cast<double*>(smem + NW * kStride + kTabBytes / 8) + 32 * warp;  // M = 5, 7
     for (uint32_t k = p.s_begin + blockIdx.x * NW + warp; k < p.s_end; k += gridDim.x * NW) {
         const Quota qk = quota(p, k);
-        if (qk.cnt == 0) continue;
-        if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<1>(p, k + gridDim.x * NW, lane);
+        if constexpr (kStaged) {
+            stage_wait();
+            NRNG_SYNCWARP();  // every lane's copies of stream k are visible to the warp
+            if (qk.cnt == 0) {
+                if (k + gridDim.x * NW < p.s_end) stage_state(stg, p, k + gridDim.x * NW, lane);
+                continue;
+            }
+        } else {
+            if (qk.cnt == 0) continue;
+        }
+        if constexpr (!kStaged && (M != 1 || NRNG_PREFETCH_B1)) prefetch_state<1>(p, k + gridDim.x * NW, lane);
         uint64_t* rk = p.ring + (uint64_t)k * kPitch;
         // x_{C-607+j} -> logical position 417 + j.  (Ring and counter loaded together; except in
         // B1's one-block-per-SM kernel, whose schedule came out 4% slower with it: measured.)
         auto win = [&](uint32_t j) { return buf + swz((kWin - kLagR) + j); };
         uint64_t C;
-        if constexpr (M == 1 && NW == kPwWarps) {
+        if constexpr (kStaged) {
+            C = load_state_rot(stg, stg + kPitch, lane, win);
+        } else if constexpr (M == 1 && NW == kPwWarps) {
             C = p.count[k];
             load_state(rk, C, lane, win, all_state_words);
         } else {
             C = load_state_rot(rk, p.count + k, lane, win);
         }
         NRNG_SYNCWARP();
-        if constexpr (M != 1 || NRNG_PREFETCH_B1) prefetch_state<2>(p, k + gridDim.x * NW, lane);
+        if constexpr (kStaged) {  // every lane has read the staging area: refill it with the next stream
+            if (k + gridDim.x * NW < p.s_end) stage_state(stg, p, k + gridDim.x * NW, lane);
+        } else if constexpr (M != 1 || NRNG_PREFETCH_B1) {
+            prefetch_state<2>(p, k + gridDim.x * NW, lane);
+        }
         uint64_t used;  // words consumed by this call
         if constexpr (M <= 2) {
             // pairs whose 16-byte outputs are all in range (odd n: the very last pair is not)
