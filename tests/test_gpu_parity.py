@@ -74,12 +74,8 @@ def test_p2_shard_sampled():
     out = torch.empty(c.n, dtype=torch.float64, device="cuda")
     g.normal("P2", out=out)
     per_stream = c.n // c.streams
-    counts = g.stream_counts()
-    for k in (0, 777, c.streams - 1):
-        st = O.Streams(c.seed, 1, first_stream=k)
-        o = st.normal_polar2(per_stream)
-        assert np.max(np.abs(host(out[k * per_stream:(k + 1) * per_stream]) - o)) <= TOL_APPROX
-        assert counts[k] == st.counts[0]
+    check_stream_blocks(out, c.seed, 0, per_stream, "P2", 0.0, 1.0, g.stream_counts(),
+                        sample_blocks(c.streams, 64, 16, 3))
     del out
 
 
@@ -138,40 +134,48 @@ def test_c2_polar_full():
     assert_state_equal(g, st)  # exact stop: consumed uniforms per stream bit-exact
 
 
+def check_stream_blocks(d, seed, first, per_stream, method, mu, sigma, counts, blocks):
+    """Streams [k, k + B) of a full-size call against the oracle run on exactly those streams
+    (the oracle's stream ids are global: first + k), element by element, with their counters."""
+    for k, B in blocks:
+        st = O.Streams(seed, B, first_stream=first + k)
+        o = ora_normals(st, method, B * per_stream, mu, sigma)
+        dk = host(d[k * per_stream:(k + B) * per_stream])
+        assert np.max(np.abs(dk - o)) <= tol_for(method), (method, k, B)
+        assert np.array_equal(counts[k:k + B], st.counts), (method, k, B)
+
+
+def sample_blocks(S, B, n_random, seed):
+    # the first and last B streams, B around the middle, and n_random single streams
+    rng = np.random.default_rng(seed)
+    ks = sorted(set(int(k) for k in rng.integers(B, S - 2 * B, n_random)))
+    return [(0, B), (S // 2 - B // 2, B), (S - B, B)] + [(k, 1) for k in ks]
+
+
 @pytest.mark.parametrize("method", ["B2", "B3"])
-def test_c3_full_size_sampled_streams(method):
+def test_c3_full_size_all_streams(method):
+    # 2^28 normals over 2^16 streams: all of them, every element and counter (2 GB per side)
     c = W.C3
     g = P.Generator(c.seed, c.streams)
     d = g.normal(method, c.n, c.mu, c.sigma)
     per_stream = c.n // c.streams
-    rng = np.random.default_rng(5)
-    ks = sorted(set([0, 1, c.streams - 1] + list(rng.integers(0, c.streams, 13))))
-    counts = g.stream_counts()
-    for k in ks:
-        st = O.Streams(c.seed, 1, first_stream=int(k))
-        o = ora_normals(st, method, per_stream, c.mu, c.sigma)
-        dk = host(d[k * per_stream:(k + 1) * per_stream])
-        assert np.max(np.abs(dk - o)) <= tol_for(method)
-        assert counts[k] == st.counts[0]
+    check_stream_blocks(d, c.seed, 0, per_stream, method, c.mu, c.sigma, g.stream_counts(),
+                        [(0, c.streams)])
 
 
 @pytest.mark.parametrize("method", ["B1", "B2", "B3", "P"])
-def test_c5_shard_bench_launch_sampled(method):
-    # the exact launch bench.py times: 2^31 normals over 2^16 streams (global ids of rank 1)
+def test_c5_shard_bench_launch_all_streams(method):
+    # the exact launch bench.py times: 2^31 normals over 2^16 streams (global ids of rank 1);
+    # all of them, every element and counter, in blocks of 8192 streams (2 GB of host memory
+    # per side at a time)
     c = W.C5_SHARD
     first = c.streams  # rank 1 of the sharded run
     g = P.Generator(c.seed, c.streams, first_stream=first)
     out = torch.empty(c.n, dtype=torch.float64, device="cuda")
     g.normal(method, out=out)
     per_stream = c.n // c.streams
-    ks = [0, 1, 4097, 33333, c.streams - 1]
-    counts = g.stream_counts()
-    for k in ks:
-        st = O.Streams(c.seed, 1, first_stream=first + k)
-        o = ora_normals(st, method, per_stream, c.mu, c.sigma)
-        dk = host(out[k * per_stream:(k + 1) * per_stream])
-        assert np.max(np.abs(dk - o)) <= tol_for(method)
-        assert counts[k] == st.counts[0]
+    check_stream_blocks(out, c.seed, first, per_stream, method, c.mu, c.sigma, g.stream_counts(),
+                        [(k, 8192) for k in range(0, c.streams, 8192)])
     del out
 
 
