@@ -1468,6 +1468,7 @@ __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
         uint64_t* r = p.ring + (uint64_t)k * kPitch;
         const uint32_t c0 = (uint32_t)(C % kLagR);
         uint32_t i0 = 0;  // words of the call consumed before this step
+        if constexpr (V <= 3) {
         uint32_t j = 0;   // pairs delivered
         while (j < qk.cnt) {
             // this lane's words: call-relative i0 + per l + t (per = 3 for B3, else 2)
@@ -1509,41 +1510,6 @@ __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
                     store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + lane), p.shift, p.n, x[0], y[0], p.aligned);
                 words = per * take;
                 j += take;
-            } else {
-                bool ok;
-                double x[1], y[1];
-                if constexpr (V == 6) {
-                    const uint64_t wu[1] = {w[0]}, wv[1] = {w[1]};
-                    bool okr[1];
-                    ratio_candidates<1>(wu, wv, tab, x, okr);
-                    ok = okr[0];
-                } else {
-                    PolarCand c[1];
-                    ok = polar_candidate(w[0], w[1], c[0]);
-                    if (V == 5)
-                        p2_transform<1>(c, p.tp, tab, x, y);
-                    else
-                        polar_transform<1>(c, p.tp, tab, x, y);
-                }
-                const unsigned m = __ballot_sync(kFull, ok);
-                const uint32_t need = (uint32_t)(qk.cnt - j), rank = __popc(m & lt);
-                if (ok && rank < need) {
-                    if constexpr (V == 6) {
-                        const uint64_t g = qk.off + j + rank;  // one normal per accepted candidate
-                        if (g < p.n) p.out[g - p.shift] = __fma_rn(p.tp.sigma, x[0], p.tp.mu);
-                    } else {
-                        store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + rank), p.shift, p.n, x[0], y[0], p.aligned);
-                    }
-                }
-                const uint32_t got = __popc(m);
-                if (got >= need) {  // exact stop: nothing after the need-th accept is consumed
-                    const unsigned last = __ballot_sync(kFull, ok && rank == need - 1);
-                    words = 2 * (uint32_t)__ffs(last);
-                    j += need;
-                } else {
-                    words = 64;
-                    j += got;
-                }
             }
             if ((uint32_t)(per * lane) < words) {  // write back the consumed words in place
 #pragma unroll
@@ -1551,6 +1517,78 @@ __global__ void __launch_bounds__(kMidWarps * 32) mid_kernel(BulkParams p) {
             }
             i0 += words;
             NRNG_SYNCWARP();
+        }
+        } else {
+        uint32_t j = 0;   // accepted units delivered
+        // Polar/P2/R: a lane's words of the step starting at call word s are s + 2l, s + 2l + 1;
+        // the next step's sources are loaded while this step transforms, once its ballot shows
+        // another step is needed: they are never words of this step (those are < 64 words
+        // behind; the lags are 273 and 607), so one memory latency per stream, not per step.
+        auto sources = [&](uint32_t s, uint32_t (&pa)[2], uint64_t (&xa)[2], uint64_t (&xb)[2]) {
+            uint32_t a = (c0 + s + 2 * lane) % kLagR;
+            uint32_t b = a + (kLagR - kLagS);
+            b = b >= (uint32_t)kLagR ? b - kLagR : b;
+            uint32_t pb[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                pa[t] = a;
+                pb[t] = b;
+                a = a + 1 == (uint32_t)kLagR ? 0 : a + 1;
+                b = b + 1 == (uint32_t)kLagR ? 0 : b + 1;
+            }
+#pragma unroll
+            for (int t = 0; t < 2; ++t) xa[t] = r[pa[t]], xb[t] = r[pb[t]];
+        };
+        uint32_t pa[2];
+        uint64_t xa[2], xb[2];
+        sources(0, pa, xa, xb);
+        for (;;) {
+            const uint64_t w[2] = {xa[0] + xb[0], xa[1] + xb[1]};
+            bool ok;
+            double x[1], y[1];
+            PolarCand c[1];
+            if constexpr (V == 6) {
+                const uint64_t wu[1] = {w[0]}, wv[1] = {w[1]};
+                bool okr[1];
+                ratio_candidates<1>(wu, wv, tab, x, okr);
+                ok = okr[0];
+            } else {
+                ok = polar_candidate(w[0], w[1], c[0]);
+            }
+            const unsigned m = __ballot_sync(kFull, ok);
+            const uint32_t need = (uint32_t)(qk.cnt - j), rank = __popc(m & lt), got = __popc(m);
+            const bool more = got < need;
+            uint32_t npa[2];
+            uint64_t nxa[2], nxb[2];
+            if (more) sources(i0 + 64, npa, nxa, nxb);
+            if constexpr (V == 5)
+                p2_transform<1>(c, p.tp, tab, x, y);
+            else if constexpr (V == 4)
+                polar_transform<1>(c, p.tp, tab, x, y);
+            if (ok && rank < need) {
+                if constexpr (V == 6) {
+                    const uint64_t g = qk.off + j + rank;  // one normal per accepted candidate
+                    if (g < p.n) p.out[g - p.shift] = __fma_rn(p.tp.sigma, x[0], p.tp.mu);
+                } else {
+                    store_pair(p.out, 2 * pair_slot(p, qk.off, k, j + rank), p.shift, p.n, x[0], y[0], p.aligned);
+                }
+            }
+            uint32_t words;  // words this step consumes (stores only those)
+            if (!more) {  // exact stop: nothing after the need-th accept is consumed
+                const unsigned last = __ballot_sync(kFull, ok && rank == need - 1);
+                words = 2 * (uint32_t)__ffs(last);
+                j += need;
+            } else {
+                words = 64;
+                j += got;
+            }
+            if ((uint32_t)(2 * lane) < words) r[pa[0]] = w[0], r[pa[1]] = w[1];  // write back in place
+            i0 += words;
+            NRNG_SYNCWARP();
+            if (!more) break;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) pa[t] = npa[t], xa[t] = nxa[t], xb[t] = nxb[t];
+        }
         }
         if (lane == 0) p.count[k] = C + i0;
         NRNG_SYNCWARP();
