@@ -540,6 +540,9 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
 #define NRNG_POLAR_U 4
 #endif
 constexpr int kPU = NRNG_POLAR_U;  // candidates per lane per step (32 kPU per warp)
+#ifndef NRNG_POLAR_DIRECT_SPLIT
+#define NRNG_POLAR_DIRECT_SPLIT 1  // pw_kernel: a Polar step loop specialised for in-range outputs
+#endif
 #ifndef NRNG_POLAR_SPLIT_STOP
 #define NRNG_POLAR_SPLIT_STOP 1  // pw_polar_block: the exact-stop trim only in the stream's last step
 #endif
@@ -1012,11 +1015,12 @@ __device__ __forceinline__ void pw_polar_stores(const unsigned (&m)[kPU], const 
 // quota was reached (exact stop: `used` = candidates consumed of this block).  The steady
 // path (the step does not reach the quota: every step of a stream but its last) touches no
 // mask after the ballots; the trim runs only in the last step.
-template <int M, int K, bool EP = false>
+template <int M, int K, bool EP = false, bool kDirect = false>  // kDirect: `direct` known true
 __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& tp, const Tables& tab,
                                                const BulkParams& p, const Quota& qk, double2* o, bool direct,
                                                uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt,
                                                double* scr, uint32_t k = 0) {
+    if (kDirect) direct = true;
     uint64_t wa[kPU], wb[kPU];
     pw_gen_c<kPU, K>(pp, wa, wb);
     PolarCand c[kPU];
@@ -1256,16 +1260,25 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
             double2* const o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift));
             const uint32_t cnt = (uint32_t)qk.cnt;
             uint32_t acc = 0, blocks = 0, usedc = 0;
-            for (;;) {
-                if (pw_polar_block<M, 0, EP>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
-                ++blocks;
-                if (pw_polar_block<M, 256, EP>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
-                ++blocks;
-                if (pw_polar_block<M, 512, EP>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
-                ++blocks;
-                if (pw_polar_block<M, 768, EP>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
-                ++blocks;
-            }
+            // the steps of a stream whose outputs are all in range (every stream but perhaps a
+            // call's last) run without the per-step range test
+            auto steps = [&](auto kd) {
+                constexpr bool KD = decltype(kd)::value;
+                for (;;) {
+                    if (pw_polar_block<M, 0, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
+                    ++blocks;
+                    if (pw_polar_block<M, 256, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
+                    ++blocks;
+                    if (pw_polar_block<M, 512, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
+                    ++blocks;
+                    if (pw_polar_block<M, 768, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
+                    ++blocks;
+                }
+            };
+            if (!EP && NRNG_POLAR_DIRECT_SPLIT && direct)
+                steps(std::integral_constant<bool, true>{});
+            else
+                steps(std::integral_constant<bool, false>{});
             used = (uint64_t)kBlk * blocks + 2 * usedc;
         }
         // write back the last min(used, 607) consumed words (word i at logical i mod 1024)
