@@ -547,22 +547,31 @@ Kind kind_of(int method) {
 }
 // `epochs` whole epochs into device memory dst (epoch layout).
 int seq_epochs(nrng_handle h, int method, double* dst, uint64_t epochs, double mu, double sigma) {
-    BulkParams p{};
-    p.ring = h->ring;
-    p.count = h->count;
-    p.q = epochs << h->seq.log2E;
-    p.rem = 0;
-    p.units = p.q * h->S;
-    p.n = 2 * p.units;
-    p.tp = TParams{mu, sigma, sigma * 0x1.6a09e667f3bcdp+0};
-    p.out = dst;
-    p.shift = 0;
-    p.aligned = ((uintptr_t)dst & 15) == 0;
-    p.s_begin = 0;
-    p.s_end = h->S;
-    p.log2E = h->seq.log2E;
-    p.S = h->S;
-    return cuda_err(launch_bulk(h, kind_of(method), p, h->stream));
+    // whole epochs are contiguous blocks of the epoch-major output, so a long run goes as
+    // consecutive launches of at most kPieceUnits pairs per stream (the kernels count a
+    // launch's units and words per stream in 32 bits), exact by partition invariance
+    const uint64_t max_epochs = std::max<uint64_t>(1, kPieceUnits >> h->seq.log2E);
+    const uint64_t epoch_deviates = 2ull * h->S << h->seq.log2E;
+    cudaError_t e = cudaSuccess;
+    for (uint64_t e0 = 0; e0 < epochs && e == cudaSuccess; e0 += max_epochs) {
+        BulkParams p{};
+        p.ring = h->ring;
+        p.count = h->count;
+        p.q = std::min(max_epochs, epochs - e0) << h->seq.log2E;
+        p.rem = 0;
+        p.units = p.q * h->S;
+        p.n = 2 * p.units;
+        p.tp = TParams{mu, sigma, sigma * 0x1.6a09e667f3bcdp+0};
+        p.out = dst + e0 * epoch_deviates;
+        p.shift = 0;
+        p.aligned = ((uintptr_t)p.out & 15) == 0;
+        p.s_begin = 0;
+        p.s_end = h->S;
+        p.log2E = h->seq.log2E;
+        p.S = h->S;
+        e = launch_bulk(h, kind_of(method), p, h->stream);
+    }
+    return cuda_err(e);
 }
 }  // namespace
 

@@ -126,6 +126,31 @@ def test_device_output_long_quota_pieces(method):
     del x, y, parts
 
 
+def test_sequential_mode_long_run_pieces():
+    # a device-output sequential call over few streams and many epochs: 3 x 2^30 + 768
+    # deviates from one stream are 1.5 x 2^30 + 384 B3 pairs, 4.8e9 words -- past the kernels'
+    # 32-bit per-launch word counts (round 2 found the sequential mode bypassing the pieces
+    # of run_bulk: this call failed) -- so it runs as launches of at most 2^28 pairs per
+    # stream; equal to a sequence of shorter calls (the canonical sequence is partition
+    # invariant), which the oracle-checked sequential tests pin.  One stream = one warp: ~40 s
+    method = "B3"
+    n = 3 * (1 << 30) + 768
+    free = torch.cuda.mem_get_info()[0]
+    if free < 2 * n * 8 + (4 << 30):
+        pytest.skip("not enough device memory")
+    a, b = P.Generator(5, 1), P.Generator(5, 1)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    a.normal_seq(method, out=x)
+    y = torch.empty(n, dtype=torch.float64, device="cuda")
+    step = 1 << 30
+    for s in range(0, n, step):
+        b.normal_seq(method, out=y[s:min(n, s + step)])
+    torch.cuda.synchronize()
+    assert torch.equal(x, y)
+    assert np.array_equal(a.stream_counts(), b.stream_counts())
+    del x, y
+
+
 # ---------------------------------------------------------------- 4-warp-block bulk kernels
 # fewer streams than 16 x 148 one-block-per-SM slots, > 128 units per stream (above mid_kernel)
 
