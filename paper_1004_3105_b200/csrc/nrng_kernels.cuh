@@ -470,8 +470,8 @@ __global__ void __launch_bounds__(NW * 32, 1) b3_kernel(BulkParams p) {
         double2* o = EP ? reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, 0) + lane
                         : reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;  // per-iteration
         auto adv = [&](uint32_t itn) {  // o -> the first pair of iteration itn (+ lane)
-            if constexpr (EP)
-                o = reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, 128ull * itn) + lane;
+            if constexpr (EP)  // +128 pairs inside an epoch chunk (E >= 128, 128 | E), else to the next epoch's
+                o += ((128u * itn) & ((1u << p.log2E) - 1)) ? 128 : ((uint64_t)p.S << p.log2E) - (1u << p.log2E) + 128;
             else
                 o += 128;
         };
@@ -1171,8 +1171,8 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
                             : reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift)) + lane;
             uint32_t b = 0;
             auto adv = [&](uint32_t bn) {  // o -> the first pair of block bn (+ lane)
-                if constexpr (EP)
-                    o = reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, 128ull * bn) + lane;
+                if constexpr (EP)  // +128 pairs inside an epoch chunk (E >= 128, 128 | E), else to the next epoch's
+                    o += ((128u * bn) & ((1u << p.log2E) - 1)) ? 128 : ((uint64_t)p.S << p.log2E) - (1u << p.log2E) + 128;
                 else
                     o += 128;
             };
