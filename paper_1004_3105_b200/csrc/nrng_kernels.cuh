@@ -981,19 +981,23 @@ __device__ __forceinline__ uint32_t polar_trim(const bool (&ok)[kPU], unsigned (
 template <bool EP>
 __device__ __forceinline__ void pw_polar_stores(const unsigned (&m)[kPU], const double (&ox)[kPU],
                                                 const double (&oy)[kPU], const BulkParams& p, const Quota& qk,
-                                                double2* o, bool direct, uint32_t& acc, int lane, unsigned lt,
-                                                uint32_t k) {
+                                                double2*& o, bool direct, uint32_t& acc, int lane, unsigned lt,
+                                                uint32_t& jb) {
     if (EP) {  // the sequential mode's epoch layout (whole epochs: every pair is in range)
-        // a step's <= 128 pairs span at most two epoch chunks of E >= 128 pairs: pair j goes to
-        // chunk e0's start + (j - e0 E), plus the jump to the next chunk once j - e0 E >= E
-        const uint32_t e0 = acc >> p.log2E, jb = e0 << p.log2E, E = 1u << p.log2E;
-        double2* const ob = reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, jb);
+        // o = the slot of pair jb, the first of the epoch chunk (E >= 128 pairs) holding pair
+        // acc; a step's <= 128 pairs span at most two chunks: pair j goes to o + (j - jb), plus
+        // the jump to the next chunk once j - jb >= E
+        const uint32_t E = 1u << p.log2E;
         const uint64_t jump = ((uint64_t)p.S << p.log2E) - E;
 #pragma unroll
         for (int u = 0; u < kPU; ++u) {
             const uint32_t jj = acc + __popc(m[u] & lt) - jb;
-            if ((m[u] >> lane) & 1u) __stcs(ob + jj + (jj >= E ? jump : 0), make_double2(ox[u], oy[u]));
+            if ((m[u] >> lane) & 1u) __stcs(o + jj + (jj >= E ? jump : 0), make_double2(ox[u], oy[u]));
             acc += __popc(m[u]);
+        }
+        if (acc - jb >= E) {
+            jb += E;
+            o += jump + E;
         }
     } else if (direct) {
 #pragma unroll
@@ -1017,9 +1021,9 @@ __device__ __forceinline__ void pw_polar_stores(const unsigned (&m)[kPU], const 
 // mask after the ballots; the trim runs only in the last step.
 template <int M, int K, bool EP = false, bool kDirect = false>  // kDirect: `direct` known true
 __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& tp, const Tables& tab,
-                                               const BulkParams& p, const Quota& qk, double2* o, bool direct,
+                                               const BulkParams& p, const Quota& qk, double2*& o, bool direct,
                                                uint32_t cnt, uint32_t& acc, uint32_t& used, int lane, unsigned lt,
-                                               double* scr, uint32_t k = 0) {
+                                               double* scr, uint32_t& jb) {
     if (kDirect) direct = true;
     uint64_t wa[kPU], wb[kPU];
     pw_gen_c<kPU, K>(pp, wa, wb);
@@ -1047,14 +1051,14 @@ __device__ __forceinline__ bool pw_polar_block(const PwPtrs& pp, const TParams& 
         polar_transform<kPU>(c, tp, tab, ox, oy);
 #if NRNG_POLAR_SPLIT_STOP
     if (__builtin_expect(!stop, 1)) {
-        pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, k);
+        pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, jb);
         used = 32 * kPU;
     } else {
         used = polar_trim(ok, m, cnt - acc, lt);
-        pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, k);
+        pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, jb);
     }
 #else
-    pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, k);
+    pw_polar_stores<EP>(m, ox, oy, p, qk, o, direct, acc, lane, lt, jb);
 #endif
     NRNG_SYNCWARP();
     return stop;
@@ -1257,21 +1261,22 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
         } else {
             // Polar: 128 candidates (one 4-row block) per step, ranked by ballot, exact stop (R5).
             const bool direct = 2 * (qk.off + qk.cnt) <= p.n;
-            double2* const o = reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift));
+            double2* o = EP ? reinterpret_cast<double2*>(p.out) + pair_slot(p, qk.off, k, 0)
+                            : reinterpret_cast<double2*>(p.out + (2 * qk.off - p.shift));
             const uint32_t cnt = (uint32_t)qk.cnt;
-            uint32_t acc = 0, blocks = 0, usedc = 0;
+            uint32_t acc = 0, blocks = 0, usedc = 0, jb = 0;  // jb: EP's current epoch chunk
             // the steps of a stream whose outputs are all in range (every stream but perhaps a
             // call's last) run without the per-step range test
             auto steps = [&](auto kd) {
                 constexpr bool KD = decltype(kd)::value;
                 for (;;) {
-                    if (pw_polar_block<M, 0, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
+                    if (pw_polar_block<M, 0, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, jb)) break;
                     ++blocks;
-                    if (pw_polar_block<M, 256, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
+                    if (pw_polar_block<M, 256, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, jb)) break;
                     ++blocks;
-                    if (pw_polar_block<M, 512, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
+                    if (pw_polar_block<M, 512, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, jb)) break;
                     ++blocks;
-                    if (pw_polar_block<M, 768, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, k)) break;
+                    if (pw_polar_block<M, 768, EP, KD>(pp, p.tp, tab, p, qk, o, direct, cnt, acc, usedc, lane, lt, scr, jb)) break;
                     ++blocks;
                 }
             };
