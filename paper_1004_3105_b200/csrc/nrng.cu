@@ -193,6 +193,10 @@ void launch_polar(nrng_handle h, const BulkParams& p, uint32_t ns, cudaStream_t 
         pw_kernel<4, kPwWarps, true><<<h->num_sms, kPwWarps * 32, bm_smem(kPwWarps), st>>>(p);
         return;
     }
+    if (M == 2 && NRNG_P2_PW && epoch_fast(p) && eff_qmax(p) < (1ull << 31) && ns >= (uint32_t)(kPwWarps * h->num_sms)) {
+        pw_kernel<5, kPwWarps, true><<<h->num_sms, kPwWarps * 32, pw_smem(5, true, kPwWarps), st>>>(p);
+        return;
+    }
     if (M == 2 && epoch_fast(p) && eff_qmax(p) < (1ull << 31) && ns >= (uint32_t)(kBigBlockPolar * h->num_sms)) {
         polar_kernel<kBigBlockPolar, 2, true><<<h->num_sms, kBigBlockPolar * 32, polar_smem(kBigBlockPolar), st>>>(p);
         return;
@@ -426,6 +430,7 @@ nrng_handle create_impl(uint64_t seed, uint64_t first, uint32_t S, int variant) 
     occupancy(pw_kernel<1, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
     occupancy(pw_kernel<2, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
     occupancy(pw_kernel<4, kPwWarps, true>, kPwWarps, bm_smem(kPwWarps));
+    occupancy(pw_kernel<5, kPwWarps, true>, kPwWarps, pw_smem(5, true, kPwWarps));
     occupancy(b3_kernel<kTriWarps, true>, kTriWarps, tri_smem(kTriWarps));
     h->occ.ratio = occupancy(pw_kernel<6, kWarpsPerBlock>, kWarpsPerBlock, pw_smem(6, false, kWarpsPerBlock));
     h->occ.pw[0] = occupancy(pw_kernel<4, kWarpsPerBlock>, kWarpsPerBlock, pw_smem(4, false, kWarpsPerBlock));

@@ -190,7 +190,8 @@ def test_misaligned_wide(S, method):
 
 # ---------------------------------------------------------------- sequential mode, P2 wide
 def test_sequential_p2_wide_epoch_kernel():
-    # >= 20 x 148 streams: whole P2 epochs on polar_kernel<20,2,true>
+    # >= 16 x 148 streams: whole P2 epochs on the pair-window kernel pw_kernel<5,16,true>
+    # (polar_kernel<20,2,true> only in a -DNRNG_P2_PW=0 build)
     S, E = 3000, 128
     ep = 2 * S * E
     total = 2 * ep + 999
