@@ -453,8 +453,8 @@ def main():
             "hbm_peak_gbs": hbm_w, "hbm_peak_source": hbm_src,
             "kernel": "%s (%s)" % (KERNEL[dom], dom), "method": dom, "traffic": TRAFFIC.get(dom)}
 
-    cpu = None
-    if not args.no_cpu:
+    cpu = None  # the CPU oracle is timed at N = 1 only (the contract's cpu_baseline)
+    if not args.no_cpu and world == 1:
         threads = os.cpu_count() or 1
         # calibrate on 256 streams, then size the sample for ~10 s of oracle wall time
         cv, _, _, csecs = oracle_sample(256, threads)
