@@ -127,8 +127,8 @@ int nrng_normal_ratio1(nrng_handle h, double* out, size_t n, double mu, double s
  * power of two in [128, 2^20], default 128).  nrng_normal_seq(h, out, n, ...) returns the
  * next n deviates of that sequence: it first drains the deviates left over from the last
  * partially used epoch (kept in a handle-owned device buffer of 2 S E doubles), then writes
- * whole epochs straight into `out` (one launch), then generates one more epoch into the
- * buffer for the remainder.  Any split of a total into calls gives the same concatenated
+ * whole epochs straight into `out` (one launch per at most 2^28 pairs per stream), then
+ * generates one more epoch into the buffer for the remainder.  Any split of a total into calls gives the same concatenated
  * output; odd counts and Polar's exact-count requirement need no dropped deviates.
  * EINVAL if deviates of another (method, mu, sigma) are still buffered (nrng_seq_reset
  * discards them; their uniforms stay consumed).  method: 1/2/3 = B1/B2/B3, 4 = P, 5 = P2.
