@@ -53,17 +53,17 @@ __device__ __forceinline__ uint64_t pair_slot(const BulkParams& p, uint64_t off,
 // over all SMs) and NW = kBigBlock warps, one block per SM (the tables are stored once per
 // SM instead of once per 4 warps, which is what lets 20 windows fit in 227 KB).
 constexpr size_t win_bytes(int nw) { return (size_t)nw * kWinAlloc * sizeof(uint64_t); }
-// The Polar and P2 pair-window kernels stage the warp's NEXT stream -- its ring row and counter --
-// in shared memory with cp.async while the current one computes: kStageWords after the
-// 1024-word window, in place of the mirror they do not use.  Measured (interleaved, r2y/r2z/
-// r2zp): C2 (2^14 streams of 512 pairs) P 64.3 -> 60.0 us, P2 79.6 -> 74.5 us, the bench shape
-// within noise; for B2, R and R1 it cost 1-2% at the bench shape and in C3, so they keep the
-// L2 prefetch.
+// The rejection methods' pair-window kernels (P, P2, R, R1) stage the warp's NEXT stream -- its
+// ring row and counter -- in shared memory with cp.async while the current one computes:
+// kStageWords after the 1024-word window, in place of the mirror they do not use.  Measured
+// (interleaved, r2y/r2z/r2zp/r2zs): C2 (2^14 streams) P 64.3 -> 60.0 us, P2 79.6 -> 74.5 us,
+// R 100.9 -> 96.8, R1 113.3 -> 108.8, the bench shape within noise; for B2 it cost 1-2% at the
+// bench shape and in C3, so it keeps the L2 prefetch (B1 and B3 use their mirrors).
 #ifndef NRNG_STAGE_NEXT
 #define NRNG_STAGE_NEXT 1
 #endif
 constexpr int kStageWords = kPitch + 2;  // ring row (608) + counter + pad (16-byte multiple)
-__host__ __device__ constexpr bool pw_staged(int M, bool EP) { return NRNG_STAGE_NEXT && (M == 4 || M == 5) && !EP; }
+__host__ __device__ constexpr bool pw_staged(int M, bool EP) { return NRNG_STAGE_NEXT && M >= 4 && !EP; }
 __host__ __device__ constexpr int pw_stride(int M, bool EP) { return pw_staged(M, EP) ? kWin + kStageWords : kWinAlloc; }
 constexpr size_t pw_smem(int M, bool EP, int nw) {
     return (size_t)nw * pw_stride(M, EP) * sizeof(uint64_t) + kTabBytes +
