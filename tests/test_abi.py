@@ -106,3 +106,24 @@ def test_output_buffer_checks():
         P.out_buffer(ro)
     with pytest.raises(TypeError):
         P.out_buffer([0.0] * 4)
+
+
+def c_demo_cmd(out_path, lib_path):
+    lib_dir = os.path.dirname(lib_path)
+    return ["gcc", "-std=c11", "-O2", "-Wall", "-Wextra", "-Werror", "-I" + os.path.join(ROOT, "include"),
+            os.path.join(ROOT, "examples", "c_api_demo.c"), "-L" + lib_dir, "-lnrng", "-Wl,-rpath," + lib_dir,
+            "-lm", "-o", out_path]
+
+
+def test_c_example_builds_against_the_header(libnrng, tmp_path):
+    # the header is plain C11 and the library links from a C program (no Python, no CUDA headers);
+    # tests/test_gpu_c_api.py runs the program on a GPU
+    import shutil
+
+    if shutil.which("gcc") is None:
+        pytest.skip("no gcc")
+    _, path = libnrng
+    exe = str(tmp_path / "c_api_demo")
+    res = subprocess.run(c_demo_cmd(exe, path), capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    assert os.path.exists(exe)
