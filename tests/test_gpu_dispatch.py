@@ -277,3 +277,28 @@ def test_edge_words_few_stream_kernels(aligned):
         g.normal(method, out=view, mu=-1.0, sigma=3.0)
         check(host(view), ora(st, method, n, -1.0, 3.0), method, (method, aligned))
         assert_state_equal(g, st)
+
+
+# ---------------------------------------------------------------- independent handles
+def test_two_handles_on_two_streams_concurrently():
+    # distinct handles share no state (include/nrng.h "Concurrency"): two generators enqueued
+    # alternately on two CUDA streams, their kernels free to overlap, give exactly what each
+    # gives alone; consecutive calls and a Polar call included
+    S, n = 4096, 2 * 4096 * 300
+    ref = {}
+    for seed in (3, 4):
+        g = P.Generator(seed, S)
+        ref[seed] = [host(g.normal(m, n)) for m in ("B1", "P", "B3")]
+        g.close()
+    ga, gb = P.Generator(3, S), P.Generator(4, S)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = {3: [], 4: []}
+    for m in ("B1", "P", "B3"):
+        with torch.cuda.stream(sa):
+            outs[3].append(ga.normal(m, n))
+        with torch.cuda.stream(sb):
+            outs[4].append(gb.normal(m, n))
+    torch.cuda.synchronize()
+    for seed in (3, 4):
+        for got, want in zip(outs[seed], ref[seed]):
+            assert np.array_equal(got.cpu().numpy(), want)
