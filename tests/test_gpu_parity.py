@@ -68,14 +68,15 @@ def test_c2_polar2_full():
     assert_state_equal(g, st)
 
 
-def test_p2_shard_sampled():
+def test_p2_shard_all_streams():
+    # method P2 at the bench shape (2^31 normals over 2^16 streams): every output and counter
     c = W.C5_SHARD
     g = P.Generator(c.seed, c.streams)
     out = torch.empty(c.n, dtype=torch.float64, device="cuda")
     g.normal("P2", out=out)
     per_stream = c.n // c.streams
     check_stream_blocks(out, c.seed, 0, per_stream, "P2", 0.0, 1.0, g.stream_counts(),
-                        sample_blocks(c.streams, 64, 16, 3))
+                        [(k, 8192) for k in range(0, c.streams, 8192)])
     del out
 
 
@@ -280,19 +281,24 @@ def test_ratio_bulk_parity(S, ns):
     assert_state_equal(g, st)
 
 
-def test_ratio_bench_shape_sampled_and_host_output():
+def check_ratio_blocks(out, seed, per, counts, blocks):
+    # R / R1 outputs of blocks of streams, bit for bit against the oracle's Algorithm R; the
+    # oracle's smallest decision margin over the block must exceed 1e-12 (reading R27)
+    for k, B in blocks:
+        st = O.Streams(seed, B, first_stream=k)
+        o = st.normal_ratio(B * per)
+        assert st.ratio_margin > 1e-12, (k, B, st.ratio_margin)
+        assert np.array_equal(host(out[k * per:(k + B) * per]), o), (k, B)
+        assert np.array_equal(counts[k:k + B], st.counts), (k, B)
+
+
+def test_ratio_bench_shape_all_streams_and_host_output():
+    # bench shape (2^31 normals over 2^16 streams): every output and counter, in blocks of 8192 streams
     c = W.C5_SHARD
     g = P.Generator(c.seed, c.streams)
     out = torch.empty(c.n, dtype=torch.float64, device="cuda")
     g.normal("R", out=out)
-    per = c.n // c.streams
-    counts = g.stream_counts()
-    for k in [0, 1, 777, c.streams - 1]:
-        st = O.Streams(c.seed, 1, first_stream=k)
-        o = st.normal_ratio(per)
-        assert st.ratio_margin > 1e-12
-        assert np.array_equal(host(out[k * per:(k + 1) * per]), o)
-        assert counts[k] == st.counts[0]
+    check_ratio_blocks(out, c.seed, c.n // c.streams, g.stream_counts(), [(k, 8192) for k in range(0, c.streams, 8192)])
     del out
     # host output (chunked staging, one normal per unit)
     g1, g2 = P.Generator(3, 2048), P.Generator(3, 2048)
@@ -343,19 +349,12 @@ def test_ratio1_bulk_parity(S, ns):
     assert_state_equal(g, st)
 
 
-def test_ratio1_bench_shape_sampled():
+def test_ratio1_bench_shape_all_streams():
     c = W.C5_SHARD
     g = P.Generator(c.seed, c.streams)
     out = torch.empty(c.n, dtype=torch.float64, device="cuda")
     g.normal("R1", out=out)
-    per = c.n // c.streams
-    counts = g.stream_counts()
-    for k in [0, 1, 4242, c.streams - 1]:
-        st = O.Streams(c.seed, 1, first_stream=k)
-        o = st.normal_ratio(per)
-        assert st.ratio_margin > 1e-12
-        assert np.array_equal(host(out[k * per:(k + 1) * per]), o)
-        assert counts[k] == st.counts[0]
+    check_ratio_blocks(out, c.seed, c.n // c.streams, g.stream_counts(), [(k, 8192) for k in range(0, c.streams, 8192)])
     del out
 
 
