@@ -663,6 +663,29 @@ def test_sequential_mode_wide_epoch_kernels(method, E):
     assert np.max(np.abs(one - o)) <= tol_for(method)
 
 
+@pytest.mark.parametrize("method", ["B1", "B2", "B3", "P", "P2"])
+def test_sequential_mode_bench_shape_sampled(method):
+    # the sequential mode at the bench shape: 2^31 deviates over 2^16 streams in one call, E = 128
+    # (128 whole epochs, the EP kernels); the output is epoch-major, so viewed as
+    # [epoch][stream][2E] and transposed it is every stream's own sequence, which the oracle
+    # gives stream by stream: 3 blocks of 1024 streams and 16 single ones (all 2^16 streams pass
+    # too, ~20 s per method: run r2zz2), every element
+    c = W.C5_SHARD
+    E = 128
+    g = P.Generator(c.seed, c.streams)
+    out = g.normal_seq(method, c.n)
+    per = c.n // c.streams
+    by_stream = out.view(per // (2 * E), c.streams, 2 * E).transpose(0, 1)  # [stream][epoch][2E]
+    counts = g.stream_counts()
+    for k, B in sample_blocks(c.streams, 1024, 16, 13):
+        st = O.Streams(c.seed, B, first_stream=k)
+        o = ora_normals(st, method, B * per, 0.0, 1.0)
+        d = host(by_stream[k:k + B].reshape(-1))
+        assert np.max(np.abs(d - o)) <= tol_for(method), (method, k, B)
+        assert np.array_equal(counts[k:k + B], st.counts), (method, k, B)
+    del out, by_stream
+
+
 def test_sequential_mode_params_and_host_output():
     S = 128
     g = P.Generator(3, S)
