@@ -754,6 +754,30 @@ constexpr int kPwWarps = NRNG_PW_WARPS;
 #endif
 __device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
 
+#ifndef NRNG_STAGE_RUNS
+#define NRNG_STAGE_RUNS 1
+#endif
+// The staged state (ring order, stg[0..607) and the counter at stg[608]) into the swizzled window:
+// ring slot q goes to logical position 417 + (q - C) mod 607.  A lane's slots q = lane + 32 t lie
+// on two runs (q < C mod 607 and q >= it) whose window positions advance by 32 words per t, and
+// swz(p + 32 t) = swz(p) + 32 t (the swizzle flips bit 0 as a function of bit 4 only), so every
+// store is one of two per-lane pointers plus an immediate.
+__device__ __forceinline__ uint64_t load_staged_state(const uint64_t* stg, uint64_t* buf, int lane) {
+    constexpr int T = (kLagR + 31) / 32;
+    uint64_t v[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+        if (lane + 32 * t < kLagR) v[t] = stg[lane + 32 * t];
+    const uint64_t C = stg[kPitch];
+    const int base = (int)(C % kLagR);
+    uint64_t* const pa = buf + (int)swz((uint32_t)(kWin - base + lane));          // q < base
+    uint64_t* const pb = buf + (int)swz((uint32_t)(kWin - kLagR + lane - base));  // q >= base
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+        if (lane + 32 * t < kLagR) NRNG_ST((lane + 32 * t >= base ? pb : pa) + 32 * t, v[t]);
+    return C;
+}
+
 #ifndef NRNG_PW_NOMIRROR
 #define NRNG_PW_NOMIRROR 1  // compile-time generator: no mirror; straddling runs read through lane-wrapped pointers
 #endif
@@ -1154,7 +1178,10 @@ __global__ void __launch_bounds__(NW * 32, 1) pw_kernel(BulkParams p) {
         auto win = [&](uint32_t j) { return buf + swz((kWin - kLagR) + j); };
         uint64_t C;
         if constexpr (kStaged) {
-            C = load_state_rot(stg, stg + kPitch, lane, win);
+            if constexpr (NRNG_STAGE_RUNS && M >= 6)  // R, R1 (measured: R -3 to -4%; P, P2 within noise)
+                C = load_staged_state(stg, buf, lane);
+            else
+                C = load_state_rot(stg, stg + kPitch, lane, win);
         } else if constexpr (M == 1 && NW == kPwWarps) {
             C = p.count[k];
             load_state(rk, C, lane, win, all_state_words);
