@@ -80,6 +80,41 @@ __device__ __forceinline__ void stage_state(uint64_t* stg, const BulkParams& p, 
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 __device__ __forceinline__ void stage_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// The pair window's XOR swizzle (see pw_kernel): logical word p at physical word swz(p).
+__device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
+
+#ifndef NRNG_STAGE_RUNS
+#define NRNG_STAGE_RUNS 1
+#endif
+// A stream's state into its window: src = the ring row in ring order (global memory, or the
+// staging copy), cnt = its counter C; ring slot q holds word j = (q - C) mod 607 of the state,
+// which goes to buf + phys(W - 607 + j), phys = the pair window's swizzle (kSwz) or the identity.
+// A lane's slots q = lane + 32 t lie on two runs (q < C mod 607 and q >= it) whose window
+// positions advance by 32 words per t, and swz(p + 32 t) = swz(p) + 32 t (the swizzle flips bit 0
+// as a function of bit 4 only), so every store is one of two per-lane pointers plus an immediate.
+template <bool kSwz, int W>
+__device__ __forceinline__ uint64_t load_state_runs(const uint64_t* __restrict__ src, const uint64_t* cnt,
+                                                    uint64_t* buf, int lane) {
+    constexpr int T = (kLagR + 31) / 32;
+    uint64_t v[T];
+    const uint64_t C = *cnt;
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+        if (lane + 32 * t < kLagR) v[t] = src[lane + 32 * t];
+    const int base = (int)(C % kLagR);
+    auto phys = [](int p) { return kSwz ? (int)swz((uint32_t)p) : p; };
+    uint64_t* const pa = buf + phys(W - base + lane);          // q < base: j = q + 607 - base
+    uint64_t* const pb = buf + phys(W - kLagR + lane - base);  // q >= base: j = q - base
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+        if (lane + 32 * t < kLagR) NRNG_ST((lane + 32 * t >= base ? pb : pa) + 32 * t, v[t]);
+    return C;
+}
+__device__ __forceinline__ uint64_t load_staged_state(const uint64_t* stg, uint64_t* buf, int lane) {
+    return load_state_runs<true, kWin>(stg, stg + kPitch, buf, lane);
+}
+
 #ifndef NRNG_BIGBLOCK
 #define NRNG_BIGBLOCK 20
 #endif
@@ -752,31 +787,6 @@ constexpr int kPwWarps = NRNG_PW_WARPS;
 #ifndef NRNG_B1_MIRROR_BRANCH
 #define NRNG_B1_MIRROR_BRANCH 1
 #endif
-__device__ __forceinline__ uint32_t swz(uint32_t p) { return p ^ ((p >> 4) & 1u); }
-
-#ifndef NRNG_STAGE_RUNS
-#define NRNG_STAGE_RUNS 1
-#endif
-// The staged state (ring order, stg[0..607) and the counter at stg[608]) into the swizzled window:
-// ring slot q goes to logical position 417 + (q - C) mod 607.  A lane's slots q = lane + 32 t lie
-// on two runs (q < C mod 607 and q >= it) whose window positions advance by 32 words per t, and
-// swz(p + 32 t) = swz(p) + 32 t (the swizzle flips bit 0 as a function of bit 4 only), so every
-// store is one of two per-lane pointers plus an immediate.
-__device__ __forceinline__ uint64_t load_staged_state(const uint64_t* stg, uint64_t* buf, int lane) {
-    constexpr int T = (kLagR + 31) / 32;
-    uint64_t v[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t)
-        if (lane + 32 * t < kLagR) v[t] = stg[lane + 32 * t];
-    const uint64_t C = stg[kPitch];
-    const int base = (int)(C % kLagR);
-    uint64_t* const pa = buf + (int)swz((uint32_t)(kWin - base + lane));          // q < base
-    uint64_t* const pb = buf + (int)swz((uint32_t)(kWin - kLagR + lane - base));  // q >= base
-#pragma unroll
-    for (int t = 0; t < T; ++t)
-        if (lane + 32 * t < kLagR) NRNG_ST((lane + 32 * t >= base ? pb : pa) + 32 * t, v[t]);
-    return C;
-}
 
 #ifndef NRNG_PW_NOMIRROR
 #define NRNG_PW_NOMIRROR 1  // compile-time generator: no mirror; straddling runs read through lane-wrapped pointers
