@@ -17,6 +17,7 @@ import argparse
 import json
 import math
 import os
+import shutil
 import subprocess
 import sys
 import tempfile
@@ -85,22 +86,40 @@ class Clocks:
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
+        # started before the warm-up (nvidia-smi takes ~0.1-0.3 s to emit its first row, longer
+        # than a short timed region), line-buffered so the rows written during the timed region
+        # can be told apart (mark() / stop())
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.start_row = 0
+        cmd = ["nvidia-smi", "-i", str(index), "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+               "-lms", "50"]
+        if shutil.which("stdbuf"):
+            cmd = ["stdbuf", "-oL"] + cmd
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), "--query-gpu=" + self.FIELDS,
-                                       "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
-                                      stderr=subprocess.DEVNULL)
+            self.p = subprocess.Popen(cmd, stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+        t0 = time.time()
+        while self.p is not None and time.time() - t0 < 3.0 and not self._rows():
+            time.sleep(0.02)
+
+    def _rows(self):
+        with open(self.f.name) as fh:
+            return [r.split(",") for r in fh.read().strip().splitlines() if r.strip()]
+
+    def mark(self):
+        """Start of the timed region: rows before this one are the warm-up's."""
+        self.start_row = len(self._rows()) if self.p is not None else 0
 
     def stop(self):
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)  # one more sampling period, so the timed region's last rows are written
         self.p.terminate()
         self.p.wait()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        allrows = self._rows()
         os.unlink(self.f.name)
+        rows = allrows[self.start_row:] or allrows[-3:]  # the timed region's rows (else the last ones)
         sm = [float(r[0]) for r in rows if len(r) >= 8 and r[0].strip().replace(".", "").isdigit()]
         mx = [float(r[1]) for r in rows if len(r) >= 8 and r[1].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -113,7 +132,8 @@ class Clocks:
                     reasons.add(nm)
         loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
         return {"sm_mhz": float(np.median(loaded)) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "reasons": sorted(reasons), "samples": len(rows),
+                "samples_in_timed_region": len(allrows) - self.start_row}
 
 
 def cpu_model():
@@ -320,15 +340,16 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = Clocks(local)
     for _ in range(args.warmup):
         step()
     barrier()
-    clocks = Clocks(local)
     launches0 = g.kernel_launches
     evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in METHODS]
            for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    clocks.mark()
     start.record(stream)
     for s in range(args.steps):
         step(evs[s])
